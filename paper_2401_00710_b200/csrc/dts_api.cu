@@ -1,0 +1,1012 @@
+// dts_api.cu — C ABI (include/dts.h) and the level-synchronous MSD scheduler.
+//
+// The scheduler replaces the reference's recursive driver
+// (dtsort.py:81-209, `_run` / `_sort_rec` / `_children_step`): instead of one
+// recursive call per subproblem it processes all subproblems of one MSD
+// depth together — one sample / histogram / scan / scatter launch per level
+// over every segment, one k_local_sort launch over every base-case span —
+// and reads the level's bucket boundaries back to the host once per level to
+// plan the next one.  Output is the unique stable sort, identical to the
+// reference's.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dts.h"
+#include "dts_kernels.cuh"
+
+using namespace dts;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                 \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(DTS_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+#define DTS_TRY(expr)        \
+  do {                       \
+    int rc_ = (expr);        \
+    if (rc_ != 0) return rc_; \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Tunables (B200-sized)
+// ---------------------------------------------------------------------------
+constexpr int HIST_NT = 512;
+constexpr int SCAT_NT = 256;
+constexpr int SCAT_IPT = 16;
+constexpr int SCAT_TILE = SCAT_NT * SCAT_IPT;  // 4096 records per tile
+constexpr int SAMPLE_NT = 1024;
+constexpr uint32_t GMAX_HW = 10;               // widest digit the scatter is sized for
+constexpr uint64_t BLOCK_RECORDS = 1u << 18;   // records per count-matrix row
+constexpr uint32_t COPY_CHUNK = 1u << 16;
+constexpr uint64_t SPAN_BATCH = 1u << 18;      // spans per k_local_sort launch
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+// Local-sort capacity per record width (SMEM ~ CAP*(kb+vb+2) bytes).
+inline int local_cap(int kb, int vb) { return (kb + vb) <= 8 ? 8192 : 4096; }
+
+// ---------------------------------------------------------------------------
+// Pinned host staging (grown on demand at sync points)
+// ---------------------------------------------------------------------------
+struct Pinned {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return 0;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 1 << 20);
+    want = want + want / 2;
+    if (cudaHostAlloc(&p, want, cudaHostAllocDefault) != cudaSuccess)
+      return fail(DTS_ECUDA, "cudaHostAlloc failed for pinned staging");
+    cap = want;
+    return 0;
+  }
+};
+thread_local Pinned g_pin_plan, g_pin_back, g_pin_span;
+
+int device_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+// ---------------------------------------------------------------------------
+// Launch bookkeeping: counts launches, optionally times each class with
+// CUDA events on the launching stream.
+// ---------------------------------------------------------------------------
+struct Timer {
+  cudaStream_t st;
+  bool profile;
+  dts_report* rep;
+  uint64_t launches = 0;
+  struct Ev {
+    cudaEvent_t a, b;
+    int cls;
+  };
+  std::vector<Ev> pending;
+  std::vector<cudaEvent_t> pool;
+
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void begin(int cls, Ev& ev) {
+    ev.cls = cls;
+    ev.a = ev.b = nullptr;
+    if (!profile) return;
+    ev.a = get();
+    ev.b = get();
+    cudaEventRecord(ev.a, st);
+  }
+  void end(Ev& ev, uint64_t records) {
+    ++launches;
+    if (rep) {
+      rep->kernel_launches[ev.cls] += 1;
+      rep->kernel_records[ev.cls] += records;
+    }
+    if (!profile) return;
+    cudaEventRecord(ev.b, st);
+    pending.push_back(ev);
+  }
+  void harvest() {  // call after a stream sync
+    for (auto& e : pending) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e.a, e.b);
+      if (rep) rep->kernel_ms[e.cls] += ms;
+      pool.push_back(e.a);
+      pool.push_back(e.b);
+    }
+    pending.clear();
+  }
+  ~Timer() {
+    for (auto& e : pending) {
+      pool.push_back(e.a);
+      pool.push_back(e.b);
+    }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+template <typename F>
+int set_smem(F* fn, size_t bytes) {
+  if (bytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess)
+      return fail(DTS_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  }
+  return 0;
+}
+
+template <typename F>
+int persistent_grid(F* fn, int nt, size_t smem, uint32_t nblk) {
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, nt, smem);
+  if (per < 1) per = 1;
+  const uint64_t g = (uint64_t)per * device_sms();
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(g, nblk));
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(DTS_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Meta-region bump allocator over the caller's workspace.
+// ---------------------------------------------------------------------------
+struct Bump {
+  char* base;
+  size_t cap, off = 0;
+  void* take(size_t bytes) {
+    size_t o = align256(off);
+    if (o + bytes > cap) return nullptr;
+    off = o + bytes;
+    return base + o;
+  }
+};
+
+size_t meta_bytes(uint64_t n) { return (size_t(48) << 20) + (size_t)(n / 4); }
+
+struct HostSeg {
+  uint64_t offset, len;
+  uint32_t consumed;
+  bool root;
+};
+
+// Flat exclusive scan of `e` u32 counts into u64 offsets.
+int flat_scan(const uint32_t* cnt, uint64_t e, uint64_t* out, uint64_t* partial, Timer& tm) {
+  if (e == 0) return 0;
+  const uint64_t nch = (e + SCAN_CHUNK - 1) / SCAN_CHUNK;
+  Timer::Ev ev;
+  tm.begin(DTS_K_SCAN, ev);
+  k_scan_reduce<<<(unsigned)nch, SCAN_NT, 0, tm.st>>>(cnt, e, partial);
+  k_scan_spine<<<1, 1024, 0, tm.st>>>(partial, (uint32_t)nch);
+  k_scan_down<<<(unsigned)nch, SCAN_NT, 0, tm.st>>>(cnt, e, partial, out);
+  tm.end(ev, e);
+  tm.launches += 2;
+  return check_launch("k_scan");
+}
+
+// ---------------------------------------------------------------------------
+// The sort
+// ---------------------------------------------------------------------------
+template <typename K, int VB>
+struct Sorter {
+  using V = typename ValOf<VB>::T;
+  static constexpr int W = sizeof(K) * 8;
+
+  K* Ak;
+  V* Av;
+  K* Tk;
+  V* Tv;
+  uint64_t n;
+  Bump meta;
+  dts_config cfg;
+  dts_report* rep;
+  Timer& tm;
+  cudaStream_t st;
+
+  int cap;        // local-sort capacity (records)
+  uint64_t thr;   // base-case threshold (records <= thr -> k_local_sort)
+  uint32_t gcap, glo;
+  uint32_t stride;  // ceil_log2(n) (sampler.py:121-127)
+  uint32_t gs_max, smax;
+
+  // span / copy batches (host), flushed per level
+  std::vector<Span> spans;
+  std::vector<CopyR> copies;
+  Span cur{0, 0, 0};
+  bool have_cur = false;
+
+  Sorter(Timer& t) : tm(t) {}
+
+  uint32_t choose_gamma(uint64_t len, uint32_t remaining) const {
+    const uint64_t target = std::max<uint64_t>(1, thr / 2);
+    uint32_t need = ceil_log2_u64((len + target - 1) / target);
+    uint32_t g = std::max(need, std::min(glo, gcap));
+    g = std::min(g, gcap);
+    g = std::min(g, remaining);
+    return std::max<uint32_t>(g, 1);
+  }
+
+  void flush_span() {
+    if (have_cur && cur.len) spans.push_back(cur);
+    have_cur = false;
+  }
+  void add_span(uint64_t lo, uint64_t sz, uint32_t src) {
+    if (have_cur && cur.src == src && cur.offset + cur.len == lo && cur.len + sz <= thr) {
+      cur.len += (uint32_t)sz;
+      return;
+    }
+    flush_span();
+    cur = Span{lo, (uint32_t)sz, src};
+    have_cur = true;
+  }
+  void add_copy(uint64_t lo, uint64_t sz) {
+    for (uint64_t o = 0; o < sz; o += COPY_CHUNK) {
+      CopyR r;
+      r.offset = lo + o;
+      r.len = (uint32_t)std::min<uint64_t>(COPY_CHUNK, sz - o);
+      r.pad = 0;
+      copies.push_back(r);
+    }
+  }
+
+  int launch_spans_and_copies() {
+    flush_span();
+    if (spans.empty() && copies.empty()) return 0;
+    const size_t sb = spans.size() * sizeof(Span), cb = copies.size() * sizeof(CopyR);
+    DTS_TRY(g_pin_span.ensure(sb + cb + 512));
+    char* hp = (char*)g_pin_span.p;
+    std::memcpy(hp, spans.data(), sb);
+    std::memcpy(hp + align256(sb), copies.data(), cb);
+    // device copies of the descriptors live at the top of the meta region
+    size_t save = meta.off;
+    Span* dsp = (Span*)meta.take(std::min<size_t>(spans.size(), SPAN_BATCH) * sizeof(Span) + 16);
+    CopyR* dcp = (CopyR*)meta.take(std::min<size_t>(copies.size(), SPAN_BATCH) * sizeof(CopyR) + 16);
+    if (!dsp || !dcp) return fail(DTS_ENOMEM, "workspace too small for span descriptors");
+    const int lcap = cap;
+    for (size_t s0 = 0; s0 < spans.size(); s0 += SPAN_BATCH) {
+      const size_t cnt = std::min<size_t>(SPAN_BATCH, spans.size() - s0);
+      CUDA_TRY(cudaMemcpyAsync(dsp, hp + s0 * sizeof(Span), cnt * sizeof(Span),
+                               cudaMemcpyHostToDevice, st));
+      uint64_t recs = 0;
+      for (size_t i = s0; i < s0 + cnt; ++i) recs += spans[i].len;
+      Timer::Ev ev;
+      tm.begin(DTS_K_LOCAL, ev);
+      if (lcap == 8192) {
+        constexpr int C = 8192, NT = 512;
+        auto fn = k_local_sort<K, VB, NT, C>;
+        const size_t sm = local_layout(C, NT / 32, sizeof(K), VB).total;
+        DTS_TRY(set_smem(fn, sm));
+        fn<<<(unsigned)cnt, NT, sm, st>>>(dsp, Ak, Av, Tk, Tv);
+      } else {
+        constexpr int C = 4096, NT = 256;
+        auto fn = k_local_sort<K, VB, NT, C>;
+        const size_t sm = local_layout(C, NT / 32, sizeof(K), VB).total;
+        DTS_TRY(set_smem(fn, sm));
+        fn<<<(unsigned)cnt, NT, sm, st>>>(dsp, Ak, Av, Tk, Tv);
+      }
+      tm.end(ev, recs);
+      DTS_TRY(check_launch("k_local_sort"));
+      if (rep) {
+        rep->base_case_records += recs;
+        rep->moves += recs;
+      }
+    }
+    for (size_t c0 = 0; c0 < copies.size(); c0 += SPAN_BATCH) {
+      const size_t cnt = std::min<size_t>(SPAN_BATCH, copies.size() - c0);
+      CUDA_TRY(cudaMemcpyAsync(dcp, hp + align256(sb) + c0 * sizeof(CopyR), cnt * sizeof(CopyR),
+                               cudaMemcpyHostToDevice, st));
+      uint64_t recs = 0;
+      for (size_t i = c0; i < c0 + cnt; ++i) recs += copies[i].len;
+      Timer::Ev ev;
+      tm.begin(DTS_K_COPY, ev);
+      k_copy_ranges<K, VB><<<(unsigned)cnt, 256, 0, st>>>(dcp, Ak, Av, Tk, Tv);
+      tm.end(ev, recs);
+      DTS_TRY(check_launch("k_copy_ranges"));
+      if (rep) rep->moves += recs;
+    }
+    meta.off = save;
+    spans.clear();
+    copies.clear();
+    return 0;
+  }
+
+  // One wave: a subset of one level's segments processed by one set of launches.
+  int run_wave(const std::vector<HostSeg>& segs, size_t s0, size_t s1, int level, bool in_T,
+               std::vector<HostSeg>& next) {
+    const size_t ns = s1 - s0;
+    const bool dt = cfg.mode == DTS_MODE_DT;
+    // ---- host plans ----
+    std::vector<SegPlan> plans(ns);
+    std::vector<Blk> blks;
+    std::vector<uint32_t> sampled;
+    uint64_t cnt_total = 0, bs_total = 0, heavy_total = 0, hz_total = 0, scanbase = 0;
+    uint32_t nbc = 2, hzc = 0, hkc = 0;
+    bool any_heavy_possible = false;
+    for (size_t i = 0; i < ns; ++i) {
+      const HostSeg& hs = segs[s0 + i];
+      SegPlan& P = plans[i];
+      std::memset(&P, 0, sizeof(P));
+      const uint32_t remaining = W - hs.consumed;
+      const uint32_t g = choose_gamma(hs.len, remaining);
+      P.offset = hs.offset;
+      P.len = hs.len;
+      P.scanbase = scanbase;
+      scanbase += hs.len;
+      P.gamma = g;
+      P.shift = remaining - g;
+      P.consumed = hs.consumed;
+      P.nb = 1u << g;
+      P.nbmax = P.nb;
+      if (dt) {
+        const uint32_t gs = std::min(g, gs_max);
+        uint64_t S = std::min<uint64_t>(hs.len, (uint64_t(1) << gs) * stride);
+        S = std::min<uint64_t>(S, smax);
+        if (hs.len >= 2 * S) {
+          P.flags |= PF_SAMPLE;
+          if (hs.root && hs.consumed == 0) P.flags |= PF_ROOTSKIP;
+          P.nbmax = (1u << g) + (1u << gs) + 1u;
+          P.heavy_base = (uint32_t)heavy_total;
+          heavy_total += (1u << gs);
+          P.hz_base = (uint32_t)hz_total;
+          hz_total += (1u << g) + 1u;
+          sampled.push_back((uint32_t)i);
+          any_heavy_possible = true;
+          hzc = std::max(hzc, (1u << g) + 1u);
+          hkc = std::max(hkc, 1u << gs);
+        }
+      }
+      const uint64_t rows = std::max<uint64_t>(1, (hs.len + BLOCK_RECORDS - 1) / BLOCK_RECORDS);
+      P.nrows = (uint32_t)rows;
+      P.row0 = (uint32_t)blks.size();
+      P.cnt_base = cnt_total;
+      cnt_total += (uint64_t)P.nbmax * rows;
+      P.bs_base = (uint32_t)bs_total;
+      bs_total += P.nbmax + 1;
+      nbc = std::max(nbc, P.nbmax);
+      const uint64_t per = (hs.len + rows - 1) / rows;
+      for (uint64_t r = 0; r < rows; ++r) {
+        Blk b;
+        b.seg = (uint32_t)i;
+        b.row = (uint32_t)r;
+        b.begin = hs.offset + std::min(hs.len, r * per);
+        b.end = hs.offset + std::min(hs.len, (r + 1) * per);
+        blks.push_back(b);
+      }
+    }
+    (void)any_heavy_possible;
+    nbc = (nbc + 1) & ~1u;
+    Caps caps{nbc, hzc, hkc, 0};
+
+    // ---- device meta ----
+    const size_t save = meta.off;
+    SegPlan* dplans = (SegPlan*)meta.take(ns * sizeof(SegPlan));
+    Blk* dblks = (Blk*)meta.take(blks.size() * sizeof(Blk));
+    uint32_t* dsampled = (uint32_t*)meta.take(std::max<size_t>(1, sampled.size()) * 4);
+    uint32_t* dcnt = (uint32_t*)meta.take(cnt_total * 4);
+    uint64_t* dscan = (uint64_t*)meta.take(cnt_total * 8);
+    const uint64_t nch = (cnt_total + SCAN_CHUNK - 1) / SCAN_CHUNK;
+    uint64_t* dpart = (uint64_t*)meta.take(std::max<uint64_t>(1, nch) * 8);
+    uint64_t* dbs = (uint64_t*)meta.take(bs_total * 8);
+    uint8_t* dkinds = (uint8_t*)meta.take(bs_total);
+    K* dheavy = (K*)meta.take(std::max<uint64_t>(1, heavy_total) * sizeof(K));
+    uint32_t* dhz = (uint32_t*)meta.take(std::max<uint64_t>(1, hz_total) * 4);
+    uint32_t* dctr = (uint32_t*)meta.take(16);
+    if (!dplans || !dblks || !dsampled || !dcnt || !dscan || !dpart || !dbs || !dkinds ||
+        !dheavy || !dhz || !dctr)
+      return fail(DTS_ENOMEM, "workspace too small for level metadata");
+
+    // ---- H2D ----
+    const size_t pb = ns * sizeof(SegPlan), bb = blks.size() * sizeof(Blk),
+                 sb = sampled.size() * 4;
+    DTS_TRY(g_pin_plan.ensure(align256(pb) + align256(bb) + sb + 256));
+    char* hp = (char*)g_pin_plan.p;
+    std::memcpy(hp, plans.data(), pb);
+    std::memcpy(hp + align256(pb), blks.data(), bb);
+    if (sb) std::memcpy(hp + align256(pb) + align256(bb), sampled.data(), sb);
+    CUDA_TRY(cudaMemcpyAsync(dplans, hp, pb, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dblks, hp + align256(pb), bb, cudaMemcpyHostToDevice, st));
+    if (sb)
+      CUDA_TRY(cudaMemcpyAsync(dsampled, hp + align256(pb) + align256(bb), sb,
+                               cudaMemcpyHostToDevice, st));
+
+    const K* ink = in_T ? Tk : Ak;
+    const V* inv = in_T ? Tv : Av;
+    K* outk = in_T ? Ak : Tk;
+    V* outv = in_T ? Av : Tv;
+    uint64_t wave_recs = 0;
+    for (size_t i = 0; i < ns; ++i) wave_recs += plans[i].len;
+
+    // ---- sample + plan ----
+    if (!sampled.empty()) {
+      Timer::Ev ev;
+      tm.begin(DTS_K_SAMPLE, ev);
+      auto fn = k_sample_plan<K, SAMPLE_NT>;
+      const size_t sm = (size_t)smax * sizeof(K);
+      DTS_TRY(set_smem(fn, sm));
+      fn<<<(unsigned)sampled.size(), SAMPLE_NT, sm, st>>>(dplans, dsampled, ink, dheavy, dhz,
+                                                           cfg.seed, (uint32_t)level, stride,
+                                                           gs_max, smax);
+      tm.end(ev, sampled.size());
+      DTS_TRY(check_launch("k_sample_plan"));
+    }
+    // ---- histogram ----
+    {
+      CUDA_TRY(cudaMemsetAsync(dctr, 0, 16, st));
+      Timer::Ev ev;
+      tm.begin(DTS_K_HIST, ev);
+      auto fn = k_histogram<K, HIST_NT, false>;
+      const size_t sm = hist_layout(sizeof(K), caps, false).total;
+      DTS_TRY(set_smem(fn, sm));
+      const int grid = persistent_grid(fn, HIST_NT, sm, (uint32_t)blks.size());
+      fn<<<grid, HIST_NT, sm, st>>>(dplans, dblks, (uint32_t)blks.size(), dctr, ink, dcnt, dheavy,
+                                    dhz, nullptr, 0, caps);
+      tm.end(ev, wave_recs);
+      DTS_TRY(check_launch("k_histogram"));
+    }
+    DTS_TRY(flat_scan(dcnt, cnt_total, dscan, dpart, tm));
+    {
+      Timer::Ev ev;
+      tm.begin(DTS_K_BOUNDS, ev);
+      k_bucket_bounds<<<(unsigned)ns, 256, 0, st>>>(dplans, dscan, dhz, dbs, dkinds);
+      tm.end(ev, bs_total);
+      DTS_TRY(check_launch("k_bucket_bounds"));
+    }
+    // ---- scatter ----
+    {
+      CUDA_TRY(cudaMemsetAsync(dctr + 1, 0, 4, st));
+      Timer::Ev ev;
+      tm.begin(DTS_K_SCATTER, ev);
+      auto fn = k_scatter<K, VB, SCAT_NT, SCAT_IPT, false>;
+      const size_t sm = scatter_layout(SCAT_TILE, SCAT_NT / 32, sizeof(K), VB, caps, false).total;
+      DTS_TRY(set_smem(fn, sm));
+      const int grid = persistent_grid(fn, SCAT_NT, sm, (uint32_t)blks.size());
+      fn<<<grid, SCAT_NT, sm, st>>>(dplans, dblks, (uint32_t)blks.size(), dctr + 1, ink, inv,
+                                    outk, outv, dscan, dheavy, dhz, nullptr, 0, caps);
+      tm.end(ev, wave_recs);
+      DTS_TRY(check_launch("k_scatter"));
+    }
+    // ---- read back ----
+    DTS_TRY(g_pin_back.ensure(align256(pb) + align256(bs_total * 8) + bs_total + 256));
+    char* bp = (char*)g_pin_back.p;
+    CUDA_TRY(cudaMemcpyAsync(bp, dplans, pb, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(bp + align256(pb), dbs, bs_total * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(bp + align256(pb) + align256(bs_total * 8), dkinds, bs_total,
+                             cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    tm.harvest();
+    meta.off = save;
+    const SegPlan* rp = (const SegPlan*)bp;
+    const uint64_t* rbs = (const uint64_t*)(bp + align256(pb));
+    const uint8_t* rk = (const uint8_t*)(bp + align256(pb) + align256(bs_total * 8));
+
+    // ---- classify buckets (dtsort.py:244-318 _children_step) ----
+    const uint32_t out_src = in_T ? 0u : 1u;  // where the scatter wrote
+    if (rep) {
+      rep->moves += wave_recs;
+      rep->records_distributed += wave_recs;
+      rep->levels = std::max(rep->levels, level + 1);
+    }
+    for (size_t i = 0; i < ns; ++i) {
+      const SegPlan& P = rp[i];
+      if (rep && level == 0 && (P.flags & PF_OVF))
+        rep->skipped_bits = (int32_t)(W - (P.shift + P.gamma));
+      const uint64_t* bs = rbs + P.bs_base;
+      const uint8_t* kd = rk + P.bs_base;
+      for (uint32_t b = 0; b < P.nb; ++b) {
+        const uint64_t lo = P.offset + bs[b], hi = P.offset + bs[b + 1];
+        if (hi <= lo) continue;
+        const uint64_t sz = hi - lo;
+        const uint8_t kind = kd[b];
+        const uint32_t rem = kind == KIND_OVF ? (uint32_t)W : (kind == KIND_HEAVY ? 0u : P.shift);
+        if (rem == 0) {
+          if (rep && kind == KIND_HEAVY && level < 64) rep->heavy_records_removed[level] += sz;
+          if (out_src == 1) {
+            if (sz <= thr) add_span(lo, sz, 1);
+            else {
+              flush_span();
+              add_copy(lo, sz);
+            }
+          } else {
+            flush_span();
+          }
+          continue;
+        }
+        if (rep && level + 1 < 64) rep->level_mass[level + 1] += sz;
+        if (sz <= thr) {
+          add_span(lo, sz, out_src);
+        } else {
+          flush_span();
+          next.push_back(HostSeg{lo, sz, (uint32_t)W - rem, false});
+        }
+      }
+    }
+    return launch_spans_and_copies();
+  }
+
+  size_t wave_meta_bytes(const HostSeg& s) const {
+    const uint64_t rows = std::max<uint64_t>(1, (s.len + BLOCK_RECORDS - 1) / BLOCK_RECORDS);
+    const uint32_t g = choose_gamma(s.len, W - s.consumed);
+    const uint64_t nbmax = (1u << g) + (1u << std::min(g, gs_max)) + 1u;
+    return 88 + rows * 24 + nbmax * rows * 12 + (nbmax + 1) * 9 + (1u << g) * 12 + 4096;
+  }
+
+  int run() {
+    if (n <= 1) return 0;
+    if (n <= thr) {
+      add_span(0, n, 0);
+      return launch_spans_and_copies();
+    }
+    std::vector<HostSeg> segs{HostSeg{0, n, 0, true}};
+    if (rep) rep->level_mass[0] = n;
+    int level = 0;
+    bool in_T = false;
+    // the span/copy descriptor area must stay available after a wave
+    const size_t budget = meta.cap / 2;
+    while (!segs.empty()) {
+      std::vector<HostSeg> next;
+      size_t s0 = 0;
+      while (s0 < segs.size()) {
+        size_t s1 = s0, need = 1 << 16;
+        while (s1 < segs.size()) {
+          const size_t b = wave_meta_bytes(segs[s1]);
+          if (s1 > s0 && need + b > budget) break;
+          need += b;
+          ++s1;
+        }
+        DTS_TRY(run_wave(segs, s0, s1, level, in_T, next));
+        s0 = s1;
+      }
+      segs.swap(next);
+      in_T = !in_T;
+      ++level;
+      if (level > 200) return fail(DTS_ECUDA, "MSD recursion did not terminate");
+    }
+    return 0;
+  }
+};
+
+template <typename K, int VB>
+int sort_impl(void* keys, void* vals, uint64_t n, void* ws, size_t wsb, const dts_config* cfg,
+              dts_report* rep, cudaStream_t st) {
+  using V = typename ValOf<VB>::T;
+  Timer tm;
+  tm.st = st;
+  tm.profile = cfg->profile != 0;
+  tm.rep = rep;
+  Sorter<K, VB> S(tm);
+  S.Ak = (K*)keys;
+  S.Av = (V*)vals;
+  char* w = (char*)ws;
+  const size_t kbytes = align256(n * sizeof(K)), vbytes = align256(n * (size_t)VB);
+  S.Tk = (K*)w;
+  S.Tv = VB ? (V*)(w + kbytes) : nullptr;
+  S.meta.base = w + kbytes + vbytes;
+  S.meta.cap = wsb - kbytes - vbytes;
+  S.n = n;
+  S.cfg = *cfg;
+  S.rep = rep;
+  S.st = st;
+  S.cap = local_cap(sizeof(K), VB);
+  const int cap_env = env_int("DTS_LOCAL_CAP", 0);
+  if (cap_env == 4096 || cap_env == 8192) S.cap = cap_env;
+  // theta: SortConfig.effective_theta (core.py:148-151), capped by SMEM.
+  uint64_t theta = cfg->base_case_threshold;
+  uint32_t gcap = std::min<uint32_t>((uint32_t)std::max(1, cfg->gamma_hi),
+                                     (uint32_t)env_int("DTS_GMAX", GMAX_HW));
+  gcap = std::max<uint32_t>(1, std::min<uint32_t>(gcap, 12));
+  if (cfg->theory_mode) {
+    const uint64_t e = (uint64_t)std::max(1, cfg->base_case_exponent) * gcap;
+    theta = e >= 63 ? ~0ull : (1ull << e);
+  }
+  // reference: n_sub < theta -> base case, i.e. base case holds <= theta-1
+  uint64_t thr = theta > 0 ? theta - 1 : 0;
+  thr = std::min<uint64_t>(thr, (uint64_t)S.cap);
+  if (thr < 1) thr = 1;
+  S.thr = thr;
+  S.gcap = gcap;
+  S.glo = (uint32_t)std::max(1, cfg->gamma_lo);
+  S.stride = n <= 2 ? 1 : ceil_log2_u64(n);
+  S.gs_max = sizeof(K) == 4 ? 10 : 9;
+  S.smax = sizeof(K) == 4 ? 32768 : 16384;
+  int rc = S.run();
+  if (rc == 0) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(DTS_ECUDA, std::string("sort: ") + cudaGetErrorString(e));
+  }
+  tm.harvest();
+  if (rep) rep->gpu_launches += tm.launches;
+  return rc;
+}
+
+// ---------------------------------------------------------------------------
+// Partition (multi-GPU key-range exchange)
+// ---------------------------------------------------------------------------
+template <typename K, int VB>
+int partition_impl(const void* keys, const void* vals, uint64_t n, uint64_t gbase,
+                   const void* split_keys, const uint64_t* split_idx, int nsplit, void* okeys,
+                   void* ovals, uint64_t* counts, void* ws, size_t wsb, cudaStream_t st) {
+  using V = typename ValOf<VB>::T;
+  const uint32_t G = (uint32_t)nsplit + 1;
+  if (n == 0) {
+    for (uint32_t g = 0; g < G; ++g) counts[g] = 0;
+    return 0;
+  }
+  Timer tm;
+  tm.st = st;
+  tm.profile = false;
+  tm.rep = nullptr;
+  Bump meta{(char*)ws, wsb, 0};
+  const uint64_t rows = std::max<uint64_t>(1, (n + BLOCK_RECORDS - 1) / BLOCK_RECORDS);
+  SegPlan P;
+  std::memset(&P, 0, sizeof(P));
+  P.offset = 0;
+  P.len = n;
+  P.nb = G;
+  P.nbmax = G;
+  P.flags = PF_SPLIT;
+  P.nheavy = (uint32_t)nsplit;
+  P.nrows = (uint32_t)rows;
+  std::vector<Blk> blks;
+  const uint64_t per = (n + rows - 1) / rows;
+  for (uint64_t r = 0; r < rows; ++r)
+    blks.push_back(Blk{0, (uint32_t)r, std::min(n, r * per), std::min(n, (r + 1) * per)});
+  const uint64_t cnt_total = (uint64_t)G * rows;
+  SegPlan* dplan = (SegPlan*)meta.take(sizeof(SegPlan));
+  Blk* dblks = (Blk*)meta.take(blks.size() * sizeof(Blk));
+  uint32_t* dcnt = (uint32_t*)meta.take(cnt_total * 4);
+  uint64_t* dscan = (uint64_t*)meta.take(cnt_total * 8);
+  uint64_t* dpart = (uint64_t*)meta.take(((cnt_total + SCAN_CHUNK - 1) / SCAN_CHUNK + 1) * 8);
+  uint64_t* dbs = (uint64_t*)meta.take((G + 1) * 8);
+  uint8_t* dkinds = (uint8_t*)meta.take(G + 1);
+  K* dsk = (K*)meta.take(std::max(1, nsplit) * sizeof(K));
+  uint64_t* dsi = (uint64_t*)meta.take(std::max(1, nsplit) * 8);
+  uint32_t* dctr = (uint32_t*)meta.take(16);
+  if (!dplan || !dblks || !dcnt || !dscan || !dpart || !dbs || !dkinds || !dsk || !dsi || !dctr)
+    return fail(DTS_ENOMEM, "workspace too small for partition metadata");
+  const size_t bb = blks.size() * sizeof(Blk);
+  DTS_TRY(g_pin_plan.ensure(512 + align256(bb) + 16 * (size_t)(nsplit + 1)));
+  char* hp = (char*)g_pin_plan.p;
+  std::memcpy(hp, &P, sizeof(P));
+  std::memcpy(hp + 256, blks.data(), bb);
+  char* hs = hp + 256 + align256(bb);
+  if (nsplit) {
+    std::memcpy(hs, split_keys, nsplit * sizeof(K));
+    std::memcpy(hs + align256(nsplit * sizeof(K)), split_idx, nsplit * 8);
+  }
+  CUDA_TRY(cudaMemcpyAsync(dplan, hp, sizeof(P), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(dblks, hp + 256, bb, cudaMemcpyHostToDevice, st));
+  if (nsplit) {
+    CUDA_TRY(cudaMemcpyAsync(dsk, hs, nsplit * sizeof(K), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dsi, hs + align256(nsplit * sizeof(K)), nsplit * 8,
+                             cudaMemcpyHostToDevice, st));
+  }
+  Caps caps{(G + 1) & ~1u, 0, (uint32_t)std::max(2, nsplit + (nsplit & 1)), 0};
+  CUDA_TRY(cudaMemsetAsync(dctr, 0, 16, st));
+  {
+    auto fn = k_histogram<K, HIST_NT, true>;
+    const size_t sm = hist_layout(sizeof(K), caps, true).total;
+    DTS_TRY(set_smem(fn, sm));
+    const int grid = persistent_grid(fn, HIST_NT, sm, (uint32_t)blks.size());
+    fn<<<grid, HIST_NT, sm, st>>>(dplan, dblks, (uint32_t)blks.size(), dctr, (const K*)keys, dcnt,
+                                  dsk, nullptr, dsi, gbase, caps);
+    DTS_TRY(check_launch("k_histogram(split)"));
+  }
+  DTS_TRY(flat_scan(dcnt, cnt_total, dscan, dpart, tm));
+  k_bucket_bounds<<<1, 256, 0, st>>>(dplan, dscan, nullptr, dbs, dkinds);
+  DTS_TRY(check_launch("k_bucket_bounds(split)"));
+  {
+    auto fn = k_scatter<K, VB, SCAT_NT, SCAT_IPT, true>;
+    const size_t sm = scatter_layout(SCAT_TILE, SCAT_NT / 32, sizeof(K), VB, caps, true).total;
+    DTS_TRY(set_smem(fn, sm));
+    const int grid = persistent_grid(fn, SCAT_NT, sm, (uint32_t)blks.size());
+    fn<<<grid, SCAT_NT, sm, st>>>(dplan, dblks, (uint32_t)blks.size(), dctr + 1, (const K*)keys,
+                                  (const V*)vals, (K*)okeys, (V*)ovals, dscan, dsk, nullptr, dsi,
+                                  gbase, caps);
+    DTS_TRY(check_launch("k_scatter(split)"));
+  }
+  DTS_TRY(g_pin_back.ensure((G + 1) * 8 + 256));
+  CUDA_TRY(cudaMemcpyAsync(g_pin_back.p, dbs, (G + 1) * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  const uint64_t* bs = (const uint64_t*)g_pin_back.p;
+  for (uint32_t g = 0; g < G; ++g) counts[g] = bs[g + 1] - bs[g];
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Dovetail merge (dtmerge.py:132-238): layout on the GPU, the reference's
+// piece loop on the host, every move / reversal a grid-parallel kernel.
+// ---------------------------------------------------------------------------
+template <typename K, int VB>
+int merge_impl(void* zk_, void* zv_, uint64_t total, uint64_t light, const void* hkeys_,
+               const int64_t* hlens, uint64_t m, void* sk_, void* sv_, uint64_t scratch_len,
+               int validate, uint64_t stats[3], cudaStream_t st) {
+  using V = typename ValOf<VB>::T;
+  K* zk = (K*)zk_;
+  V* zv = (V*)zv_;
+  K* sk = (K*)sk_;
+  V* sv = (V*)sv_;
+  const K* hkeys = (const K*)hkeys_;
+  const bool has_pay = VB != 0 && zv != nullptr;
+  stats[0] = stats[1] = stats[2] = 0;
+  int64_t heavy_total_s = 0;
+  for (uint64_t i = 0; i < m; ++i) heavy_total_s += hlens[i];
+  const uint64_t heavy_total = heavy_total_s < 0 ? 0 : (uint64_t)heavy_total_s;
+  const uint64_t small = std::min<uint64_t>(light, heavy_total);
+  if (scratch_len < small)
+    return fail(DTS_EINVAL, "scratch holds " + std::to_string(scratch_len) + " records, need " +
+                                std::to_string(small));
+  if (has_pay && sv == nullptr && small > 0) return fail(DTS_EINVAL, "scratch payloads too small");
+  if (validate) {
+    if ((int64_t)light + heavy_total_s != (int64_t)total)
+      return fail(DTS_EINVAL, "light_len plus heavy run lengths must tile the zone");
+    for (uint64_t i = 0; i < m; ++i)
+      if (hlens[i] < 0) return fail(DTS_EINVAL, "heavy run lengths must be nonnegative");
+    for (uint64_t i = 1; i < m; ++i)
+      if (!(hkeys[i] > hkeys[i - 1]))
+        return fail(DTS_EINVAL, "heavy keys must be strictly increasing");
+  } else {
+    for (uint64_t i = 0; i < m; ++i)
+      if (hlens[i] < 0) return fail(DTS_EINVAL, "heavy run lengths must be nonnegative");
+    if (light + heavy_total != total)
+      return fail(DTS_EINVAL, "light_len plus heavy run lengths must tile the zone");
+  }
+  if (m == 0 || total == 0) {
+    if (validate && light > 1) {
+      // still validate light sortedness (dtmerge.py:119-121)
+    } else {
+      return 0;
+    }
+  }
+  std::vector<uint64_t> prefix(m + 1, 0);
+  for (uint64_t i = 0; i < m; ++i) prefix[i + 1] = prefix[i] + (uint64_t)hlens[i];
+  std::vector<uint64_t> p(m, 0);
+  K* dh = nullptr;
+  uint64_t* dtmp = nullptr;
+  uint32_t* derr = nullptr;
+  const size_t hbytes = std::max<uint64_t>(1, m) * sizeof(K);
+  const size_t tbytes = (2 * std::max<uint64_t>(1, m) + 2) * 8;
+  CUDA_TRY(cudaMallocAsync((void**)&dh, hbytes, st));
+  CUDA_TRY(cudaMallocAsync((void**)&dtmp, tbytes, st));
+  CUDA_TRY(cudaMallocAsync((void**)&derr, 16, st));
+  auto cleanup = [&]() {
+    cudaFreeAsync(dh, st);
+    cudaFreeAsync(dtmp, st);
+    cudaFreeAsync(derr, st);
+  };
+  uint64_t* dins = dtmp;
+  uint64_t* dpre = dtmp + std::max<uint64_t>(1, m);
+  if (m) {
+    CUDA_TRY(cudaMemcpyAsync(dh, hkeys, m * sizeof(K), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dpre, prefix.data(), m * 8, cudaMemcpyHostToDevice, st));
+    k_merge_layout<K><<<(unsigned)((m + 255) / 256), 256, 0, st>>>(zk, light, dh, m, dins);
+    if (check_launch("k_merge_layout")) {
+      cleanup();
+      return DTS_ECUDA;
+    }
+  }
+  if (validate) {
+    CUDA_TRY(cudaMemsetAsync(derr, 0, 4, st));
+    const uint64_t work = std::max<uint64_t>(total, m);
+    const unsigned grid = (unsigned)std::min<uint64_t>(4096, (work + 255) / 256 + 1);
+    k_merge_validate<K><<<grid, 256, 0, st>>>(zk, light, total, dh, dpre, m, dins, derr);
+    if (check_launch("k_merge_validate")) {
+      cleanup();
+      return DTS_ECUDA;
+    }
+    uint32_t err = 0;
+    CUDA_TRY(cudaMemcpyAsync(&err, derr, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (err) {
+      cleanup();
+      if (err & 1u) return fail(DTS_EINVAL, "light run must be sorted");
+      if (err & 2u) return fail(DTS_EINVAL, "a heavy key also appears in the light run");
+      return fail(DTS_EINVAL, "heavy run contains a foreign key");
+    }
+  }
+  if (m == 0 || total == 0) {
+    cleanup();
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return 0;
+  }
+  CUDA_TRY(cudaMemcpyAsync(p.data(), dins, m * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  auto move = [&](K* dkp, V* dvp, const K* skp, const V* svp, uint64_t len) {
+    if (!len) return;
+    const unsigned grid = (unsigned)std::min<uint64_t>(8 * device_sms(), (len + 255) / 256);
+    k_move<K, VB><<<grid, 256, 0, st>>>(dkp, dvp, skp, svp, len);
+  };
+  auto rev = [&](uint64_t lo, uint64_t hi) {
+    if (hi - lo < 2) return;
+    const uint64_t half = (hi - lo) / 2;
+    const unsigned grid = (unsigned)std::min<uint64_t>(8 * device_sms(), (half + 255) / 256);
+    k_reverse<K, VB><<<grid, 256, 0, st>>>(zk, has_pay ? zv : nullptr, lo, hi);
+  };
+  auto shift_block = [&](uint64_t src, uint64_t len, uint64_t dest) -> uint64_t {
+    // dtmerge.py:81-105
+    if (len == 0 || dest == src) return 0;
+    rev(src, src + len);
+    if (dest < src) rev(dest, src + len);
+    else rev(src, dest + len);
+    return 2 * len;
+  };
+  V* zvp = has_pay ? zv : nullptr;
+  V* svp = has_pay ? sv : nullptr;
+  uint64_t out_copies = 0, in_moves = 0, restores = 0;
+  std::vector<uint64_t> bounds(m + 2);
+  bounds[0] = 0;
+  for (uint64_t i = 0; i < m; ++i) bounds[i + 1] = p[i];
+  bounds[m + 1] = light;
+  if (heavy_total >= light) {
+    move(sk, svp, zk, zvp, light);
+    out_copies += light;
+    for (uint64_t i = 0; i < m; ++i) {
+      const uint64_t ln = (uint64_t)hlens[i];
+      const uint64_t src = light + prefix[i];
+      const uint64_t dst = p[i] + prefix[i];
+      if (ln == 0 || dst == src) continue;
+      if (dst + ln <= src) {
+        move(zk + dst, zvp ? zvp + dst : nullptr, zk + src, zvp ? zvp + src : nullptr, ln);
+        in_moves += ln;
+      } else {
+        in_moves += shift_block(src, ln, dst);
+      }
+    }
+    for (uint64_t i = 0; i <= m; ++i) {
+      const uint64_t f0 = bounds[i], f1 = bounds[i + 1];
+      const uint64_t flen = f1 - f0;
+      const uint64_t dst = f0 + prefix[i];
+      if (flen == 0 || dst == f0) continue;
+      move(zk + dst, zvp ? zvp + dst : nullptr, sk + f0, svp ? svp + f0 : nullptr, flen);
+      restores += flen;
+    }
+  } else {
+    move(sk, svp, zk + light, zvp ? zvp + light : nullptr, heavy_total);
+    out_copies += heavy_total;
+    for (uint64_t i = m; i >= 1; --i) {
+      const uint64_t f0 = bounds[i], f1 = bounds[i + 1];
+      const uint64_t flen = f1 - f0;
+      const uint64_t dst = f0 + prefix[i];
+      if (flen == 0 || dst == f0) continue;
+      if (f0 + flen <= dst) {
+        move(zk + dst, zvp ? zvp + dst : nullptr, zk + f0, zvp ? zvp + f0 : nullptr, flen);
+        in_moves += flen;
+      } else {
+        in_moves += shift_block(f0, flen, dst);
+      }
+    }
+    for (uint64_t i = 0; i < m; ++i) {
+      const uint64_t ln = (uint64_t)hlens[i];
+      if (ln == 0) continue;
+      const uint64_t s0 = prefix[i];
+      const uint64_t dst = p[i] + prefix[i];
+      move(zk + dst, zvp ? zvp + dst : nullptr, sk + s0, svp ? svp + s0 : nullptr, ln);
+      restores += ln;
+    }
+  }
+  cleanup();
+  if (check_launch("dt_merge moves")) return DTS_ECUDA;
+  CUDA_TRY(cudaStreamSynchronize(st));
+  stats[0] = out_copies;
+  stats[1] = in_moves;
+  stats[2] = restores;
+  return 0;
+}
+
+bool valid_widths(int kb, int vb) { return (kb == 4 || kb == 8) && (vb == 0 || vb == 4 || vb == 8); }
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+size_t dts_workspace_bytes(uint64_t n, int key_bytes, int val_bytes) {
+  if (!valid_widths(key_bytes, val_bytes)) return 0;
+  return align256(n * (size_t)key_bytes) + align256(n * (size_t)val_bytes) + meta_bytes(n);
+}
+
+int dts_sort(void* keys, void* vals, uint64_t n, int kb, int vb, void* ws, size_t wsb,
+             const dts_config* cfg, dts_report* rep, void* stream) {
+  if (!valid_widths(kb, vb)) return fail(DTS_EINVAL, "key_bytes must be 4|8 and val_bytes 0|4|8");
+  if (!cfg) return fail(DTS_EINVAL, "cfg must not be NULL");
+  if (n && !keys) return fail(DTS_EINVAL, "keys must not be NULL");
+  if (n && vb && !vals) return fail(DTS_EINVAL, "vals must not be NULL when val_bytes > 0");
+  if (cfg->gamma_lo < 1 || cfg->gamma_lo > cfg->gamma_hi || cfg->gamma_hi > 16)
+    return fail(DTS_EINVAL, "need 1 <= gamma_lo <= gamma_hi <= 16");
+  if (rep) std::memset(rep, 0, sizeof(*rep));
+  if (n == 0) return 0;
+  if (wsb < dts_workspace_bytes(n, kb, vb))
+    return fail(DTS_ENOMEM, "workspace holds " + std::to_string(wsb) + " bytes, need " +
+                                std::to_string(dts_workspace_bytes(n, kb, vb)));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (kb == 4) {
+    if (vb == 0) return sort_impl<uint32_t, 0>(keys, vals, n, ws, wsb, cfg, rep, st);
+    if (vb == 4) return sort_impl<uint32_t, 4>(keys, vals, n, ws, wsb, cfg, rep, st);
+    return sort_impl<uint32_t, 8>(keys, vals, n, ws, wsb, cfg, rep, st);
+  }
+  if (vb == 0) return sort_impl<uint64_t, 0>(keys, vals, n, ws, wsb, cfg, rep, st);
+  if (vb == 4) return sort_impl<uint64_t, 4>(keys, vals, n, ws, wsb, cfg, rep, st);
+  return sort_impl<uint64_t, 8>(keys, vals, n, ws, wsb, cfg, rep, st);
+}
+
+int dts_merge(void* zk, void* zv, uint64_t zone_len, uint64_t light_len, const void* hkeys,
+              const int64_t* hlens, uint64_t m, void* sk, void* sv, uint64_t scratch_len, int kb,
+              int vb, int validate, uint64_t stats_out[3], void* stream) {
+  if (!valid_widths(kb, vb)) return fail(DTS_EINVAL, "key_bytes must be 4|8 and val_bytes 0|4|8");
+  if (!stats_out) return fail(DTS_EINVAL, "stats_out must not be NULL");
+  if (m && (!hkeys || !hlens)) return fail(DTS_EINVAL, "heavy_keys and heavy_lens must have equal length");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (kb == 4) {
+    if (vb == 0) return merge_impl<uint32_t, 0>(zk, zv, zone_len, light_len, hkeys, hlens, m, sk, sv, scratch_len, validate, stats_out, st);
+    if (vb == 4) return merge_impl<uint32_t, 4>(zk, zv, zone_len, light_len, hkeys, hlens, m, sk, sv, scratch_len, validate, stats_out, st);
+    return merge_impl<uint32_t, 8>(zk, zv, zone_len, light_len, hkeys, hlens, m, sk, sv, scratch_len, validate, stats_out, st);
+  }
+  if (vb == 0) return merge_impl<uint64_t, 0>(zk, zv, zone_len, light_len, hkeys, hlens, m, sk, sv, scratch_len, validate, stats_out, st);
+  if (vb == 4) return merge_impl<uint64_t, 4>(zk, zv, zone_len, light_len, hkeys, hlens, m, sk, sv, scratch_len, validate, stats_out, st);
+  return merge_impl<uint64_t, 8>(zk, zv, zone_len, light_len, hkeys, hlens, m, sk, sv, scratch_len, validate, stats_out, st);
+}
+
+int dts_partition(const void* keys, const void* vals, uint64_t n, uint64_t gbase,
+                  const void* split_keys, const uint64_t* split_idx, int nsplit, void* okeys,
+                  void* ovals, uint64_t* counts, int kb, int vb, void* ws, size_t wsb,
+                  void* stream) {
+  if (!valid_widths(kb, vb)) return fail(DTS_EINVAL, "key_bytes must be 4|8 and val_bytes 0|4|8");
+  if (nsplit < 0 || nsplit > 4095) return fail(DTS_EINVAL, "nsplit must be in [0, 4095]");
+  if (!counts) return fail(DTS_EINVAL, "send_counts must not be NULL");
+  if (nsplit && (!split_keys || !split_idx)) return fail(DTS_EINVAL, "splitters must not be NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (kb == 4) {
+    if (vb == 0) return partition_impl<uint32_t, 0>(keys, vals, n, gbase, split_keys, split_idx, nsplit, okeys, ovals, counts, ws, wsb, st);
+    if (vb == 4) return partition_impl<uint32_t, 4>(keys, vals, n, gbase, split_keys, split_idx, nsplit, okeys, ovals, counts, ws, wsb, st);
+    return partition_impl<uint32_t, 8>(keys, vals, n, gbase, split_keys, split_idx, nsplit, okeys, ovals, counts, ws, wsb, st);
+  }
+  if (vb == 0) return partition_impl<uint64_t, 0>(keys, vals, n, gbase, split_keys, split_idx, nsplit, okeys, ovals, counts, ws, wsb, st);
+  if (vb == 4) return partition_impl<uint64_t, 4>(keys, vals, n, gbase, split_keys, split_idx, nsplit, okeys, ovals, counts, ws, wsb, st);
+  return partition_impl<uint64_t, 8>(keys, vals, n, gbase, split_keys, split_idx, nsplit, okeys, ovals, counts, ws, wsb, st);
+}
+
+const char* dts_last_error(void) { return g_err.c_str(); }
+
+int dts_abi_version(void) { return DTS_ABI_VERSION; }
+
+int dts_build_arch(void) { return 100; }
+
+}  // extern "C"

@@ -1,0 +1,210 @@
+// dts_common.cuh — shared host/device descriptors and warp primitives for the
+// B200 DovetailSort hot path.  See DESIGN.md for the data layout.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dts {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// Plan flags (SegPlan::flags)
+enum : uint32_t {
+  PF_HEAVY = 1u,     // segment has heavy keys (sampler.py:177-189)
+  PF_OVF = 2u,       // overflow bucket for keys >= ovf_thr (sampler.py:192-207)
+  PF_SAMPLE = 4u,    // sample this segment on device before routing
+  PF_ROOTSKIP = 8u,  // root: skip leading zero bits seen in the sample max
+  PF_SPLIT = 16u,    // partition mode: route by (key, index) splitters
+};
+
+// Bucket kinds written for the host planner (sampler.py:103-118 descriptors)
+enum : uint8_t { KIND_LIGHT = 0, KIND_HEAVY = 1, KIND_OVF = 2, KIND_PAD = 3 };
+
+// One distribution subproblem of an MSD level (the `_sort_rec` range
+// [lo, hi) of dtsort.py:150-209 together with its BucketPlan,
+// sampler.py:49-118).  Host-written; the sample kernel rewrites the routing
+// fields of sampled segments.
+struct SegPlan {
+  uint64_t offset;    // first record (index into both buffers)
+  uint64_t len;       // records
+  uint64_t scanbase;  // sum of len of earlier segments of this level
+  uint64_t ovf_thr;   // keys >= ovf_thr go to the overflow bucket (PF_OVF)
+  uint64_t cnt_base;  // first count entry ([bucket][row] layout)
+  uint32_t shift;     // low bit of the digit
+  uint32_t gamma;     // digit width (zones = 2^gamma)
+  uint32_t nb;        // buckets in use: 2^gamma + 2*nheavy (+1 overflow)
+  uint32_t nbmax;     // column capacity reserved by the host
+  uint32_t nheavy;    // heavy keys (ascending) at heavy_pool[heavy_base..]
+  uint32_t heavy_base;
+  uint32_t hz_base;   // zone table at hz_pool[hz_base .. +2^gamma]
+  uint32_t flags;
+  uint32_t row0;      // first block row (unused by kernels, kept for debug)
+  uint32_t nrows;     // block rows of this segment
+  uint32_t consumed;  // top bits known equal across the segment
+  uint32_t bs_base;   // bucket-bounds / kinds base index (nbmax+1 entries)
+};
+static_assert(sizeof(SegPlan) == 88, "SegPlan layout");
+
+// One count-matrix row: a contiguous chunk of one segment
+// (counting.py:116-118 block bounds).
+struct Blk {
+  uint32_t seg, row;
+  uint64_t begin, end;  // absolute record indices
+};
+
+// A base-case span: adjacent buckets sorted together by full key
+// (dtsort.py:263-281 span batching, _base_sort :127-147).
+struct Span {
+  uint64_t offset;
+  uint32_t len;
+  uint32_t src;  // 0: records are in A (caller buffer), 1: in T (temporary)
+};
+
+// A finished range that must be copied T -> A (dtsort.py:111-124).
+struct CopyR {
+  uint64_t offset;
+  uint32_t len;
+  uint32_t pad;
+};
+
+// Per-launch shared-memory table capacities (host and device agree).
+struct Caps {
+  uint32_t nbc;  // bucket columns (>= max nb of any segment in the launch)
+  uint32_t hzc;  // zone-table entries
+  uint32_t hkc;  // heavy keys / splitters
+  uint32_t pad;
+};
+
+template <int VB> struct ValOf { using T = uint32_t; };
+template <> struct ValOf<8> { using T = uint64_t; };
+
+__host__ __device__ inline uint32_t ceil_log2_u64(uint64_t x) {
+  // smallest k with 2^k >= x (0 for x <= 1)
+  if (x <= 1) return 0;
+#ifdef __CUDA_ARCH__
+  return 64 - __clzll((long long)(x - 1));
+#else
+  return 64 - __builtin_clzll(x - 1);
+#endif
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Lanes of the warp whose bucket equals this lane's (warp-level multisplit
+// peer set).  `nbits` ballots, one per bucket-id bit; deterministic cost and
+// no dependence on how many distinct ids the warp holds.
+__device__ __forceinline__ uint32_t peer_mask(uint32_t b, uint32_t valid_mask,
+                                              int nbits) {
+#ifdef DTS_USE_MATCH_ANY
+  (void)nbits;
+  return __match_any_sync(FULL, b) & valid_mask;
+#else
+  uint32_t m = valid_mask;
+  for (int i = 0; i < nbits; ++i) {
+    const uint32_t bit = (b >> i) & 1u;
+    const uint32_t bal = __ballot_sync(FULL, bit);
+    m &= bit ? bal : ~bal;
+  }
+  return m;
+#endif
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// Route one key to its bucket id: overflow > heavy (exact match) > light
+// zone, with heavy keys splitting their zone's light bucket so every bucket
+// id is monotone in the key (sampler.py:76-100 precedence; the id layout is
+// the fused-dovetail layout of DESIGN.md §4).
+template <typename K>
+struct Router {
+  K ovf_thr;
+  uint32_t shift, mask, flags, nb;
+  const uint32_t* hz;
+  const K* hk;
+
+  __device__ __forceinline__ uint32_t operator()(K key) const {
+    if ((flags & PF_OVF) && key >= ovf_thr) return nb - 1;
+    const uint32_t z = (uint32_t)(key >> shift) & mask;
+    if (!(flags & PF_HEAVY)) return z;
+    const uint32_t h0 = hz[z], h1 = hz[z + 1];
+    const uint32_t base = z + 2u * h0;
+    if (h0 == h1) return base;
+    uint32_t lo = h0, hi = h1;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (hk[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return base + 2u * (lo - h0) + ((lo < h1 && hk[lo] == key) ? 1u : 0u);
+  }
+};
+
+// Partition router: destination = number of (key, index) splitters strictly
+// below the record (SURVEY.md §8e composite splitters).
+template <typename K>
+struct SplitRouter {
+  const K* sk;
+  const uint64_t* si;
+  uint32_t ns;
+  __device__ __forceinline__ uint32_t operator()(K key, uint64_t gidx) const {
+    uint32_t lo = 0, hi = ns;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      const bool less = sk[mid] < key || (sk[mid] == key && si[mid] < gidx);
+      if (less) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  }
+};
+
+// Block-wide exclusive scan of a[0..n) in shared memory (in place); returns
+// the total.  All threads of the block must call it.  `tmp` holds NT/32
+// entries.
+template <int NT, typename T>
+__device__ __forceinline__ uint32_t block_exscan(T* a, int n, uint32_t* tmp) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (n + NT - 1) / NT;
+  const int s0 = min(n, tid * per), e0 = min(n, s0 + per);
+  uint32_t sum = 0;
+  for (int i = s0; i < e0; ++i) sum += (uint32_t)a[i];
+  uint32_t x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) tmp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < NW ? tmp[lane] : 0u;
+    uint32_t incl = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane < NW) tmp[lane] = incl - w;
+    if (lane == NW - 1) tmp[NW] = incl;  // block total
+  }
+  __syncthreads();
+  uint32_t run = tmp[warp] + x - sum;
+  for (int i = s0; i < e0; ++i) {
+    const uint32_t t = (uint32_t)a[i];
+    a[i] = (T)run;
+    run += t;
+  }
+  const uint32_t total = tmp[NW];
+  __syncthreads();
+  return total;
+}
+
+}  // namespace dts

@@ -1,0 +1,128 @@
+"""The sorters: dt_sort and plain_msd_sort on the B200.
+
+Drop-in for /root/reference/pkg/src/dovetail/dtsort.py:64-108: same names,
+same in-place contract (the caller's array objects receive the result),
+same return value (None, or an InstrumentReport when cfg.instrument) and
+the same TypeError for non-RecordArray input.  The whole MSD pipeline runs
+in libdts.so (include/dts.h `dts_sort`) on the current CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+from ._device import Column, pick_device, torch_mod
+from .core import InstrumentReport, RecordArray, SortConfig
+
+__all__ = ["dt_sort", "plain_msd_sort", "make_config", "workspace_bytes"]
+
+
+def dt_sort(records: RecordArray, cfg: SortConfig | None = None) -> InstrumentReport | None:
+    """Sort ``records`` ascending by key, stably and in place (dtsort.py:64-71)."""
+    return _run(records, cfg, _lib.MODE_DT)
+
+
+def plain_msd_sort(records: RecordArray, cfg: SortConfig | None = None) -> InstrumentReport | None:
+    """The ablation: no sampling, no heavy or overflow buckets (dtsort.py:74-78)."""
+    return _run(records, cfg, _lib.MODE_PLAIN)
+
+
+def make_config(cfg: SortConfig, mode: int, profile: bool = False) -> _lib.DtsConfig:
+    if cfg.sample_rule is not None or cfg.block_policy is not None:
+        raise NotImplementedError(
+            "SortConfig.sample_rule / block_policy are Python callables and cannot run "
+            "inside the CUDA kernels; the GPU sorter uses its own sample size and block plan"
+        )
+    c = _lib.DtsConfig()
+    c.seed = int(cfg.seed)
+    c.gamma_lo = int(cfg.gamma_lo)
+    c.gamma_hi = int(cfg.gamma_hi)
+    c.base_case_threshold = int(cfg.base_case_threshold)
+    c.theory_mode = int(bool(cfg.theory_mode))
+    c.base_case_exponent = int(cfg.base_case_exponent)
+    c.mode = int(mode)
+    c.instrument = int(bool(cfg.instrument))
+    c.profile = int(bool(profile))
+    return c
+
+
+def workspace_bytes(n: int, key_bytes: int, val_bytes: int) -> int:
+    return int(_lib.lib().dts_workspace_bytes(int(n), int(key_bytes), int(val_bytes)))
+
+
+def report_from(raw: _lib.DtsReport) -> InstrumentReport:
+    rep = InstrumentReport()
+    rep.moves = int(raw.moves)
+    rep.merge_out_copies = int(raw.merge_out_copies)
+    rep.merge_in_array_moves = int(raw.merge_in_array_moves)
+    rep.levels = int(raw.levels)
+    rep.base_case_records = int(raw.base_case_records)
+    rep.skipped_bits = int(raw.skipped_bits)
+    depth = max(rep.levels + 1, 1)
+    rep.level_mass = [int(raw.level_mass[d]) for d in range(depth)]
+    rep.heavy_records_removed = [int(raw.heavy_records_removed[d]) for d in range(rep.levels)]
+    rep.records_distributed = int(raw.records_distributed)
+    rep.gpu_launches = int(raw.gpu_launches)
+    rep.kernel_ms = {k: float(raw.kernel_ms[i]) for i, k in enumerate(_lib.K_CLASSES)}
+    rep.kernel_launches = {k: int(raw.kernel_launches[i]) for i, k in enumerate(_lib.K_CLASSES)}
+    rep.kernel_records = {k: int(raw.kernel_records[i]) for i, k in enumerate(_lib.K_CLASSES)}
+    return rep
+
+
+def sort_device(keys, vals, cfg: SortConfig, mode: int, profile: bool = False,
+                workspace=None, report: bool = False) -> InstrumentReport | None:
+    """Sort contiguous CUDA tensors in place (no validation beyond widths).
+
+    ``keys``/``vals`` are torch CUDA tensors of 4/8-byte elements (any
+    integer dtype of that width; bits are treated as unsigned).  Used by the
+    public sorters, the multi-GPU driver and bench.py.
+    """
+    torch = torch_mod()
+    n = int(keys.numel())
+    kb = keys.element_size()
+    vb = 0 if vals is None else vals.element_size()
+    c = make_config(cfg, mode, profile)
+    raw = _lib.DtsReport() if (report or cfg.instrument or profile) else None
+    L = _lib.lib()
+    need = int(L.dts_workspace_bytes(n, kb, vb))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=keys.device)
+    stream = torch.cuda.current_stream(keys.device).cuda_stream
+    rc = L.dts_sort(
+        ctypes.c_void_p(keys.data_ptr()),
+        ctypes.c_void_p(0 if vals is None else vals.data_ptr()),
+        n, kb, vb,
+        ctypes.c_void_p(workspace.data_ptr()), int(workspace.numel()),
+        ctypes.byref(c),
+        ctypes.byref(raw) if raw is not None else None,
+        ctypes.c_void_p(stream),
+    )
+    _lib.check(rc)
+    return report_from(raw) if raw is not None else None
+
+
+def _run(records: RecordArray, cfg: SortConfig | None, mode: int) -> InstrumentReport | None:
+    if not isinstance(records, RecordArray):
+        raise TypeError("records must be a RecordArray")
+    cfg = cfg or SortConfig()
+    n = len(records)
+    if n == 0:
+        make_config(cfg, mode)  # same NotImplementedError contract for callables
+        if cfg.instrument:
+            rep = InstrumentReport()
+            rep.add_mass(0, 0)
+            return rep
+        return None
+    device = pick_device(records.keys, records.payloads)
+    torch = torch_mod()
+    with torch.cuda.device(device):
+        kcol = Column(records.keys, device, None)
+        vcol = Column(records.payloads, device, None) if records.payloads is not None else None
+        rep = sort_device(kcol.dev, None if vcol is None else vcol.dev, cfg, mode)
+        kcol.writeback()
+        if vcol is not None:
+            vcol.writeback()
+        torch.cuda.current_stream(device).synchronize()
+    if not cfg.instrument:
+        return None
+    return rep
