@@ -16,7 +16,7 @@
 #include <vector>
 
 #include "../../include/dts.h"
-#include "dts_kernels.cuh"
+#include "dts_sort_kernels.cuh"
 
 using namespace dts;
 
@@ -47,8 +47,11 @@ int fail(int code, const std::string& msg) {
 // ---------------------------------------------------------------------------
 constexpr int HIST_NT = 512;
 constexpr int SCAT_NT = 256;
-constexpr int SCAT_IPT = 16;
-constexpr int SCAT_TILE = SCAT_NT * SCAT_IPT;  // 4096 records per tile
+constexpr int SCAT_IPT = 17;                   // odd: conflict-free blocked SMEM reads
+constexpr int SCAT_TILE = SCAT_NT * SCAT_IPT;  // 4352 records per tile
+constexpr int LOCAL_NT = 256;
+constexpr int LOCAL_IPT = 17;
+constexpr int LOCAL_RB = 5;                    // radix bits per local-sort pass
 constexpr int SAMPLE_NT = 1024;
 constexpr uint32_t GMAX_HW = 10;               // widest digit the scatter is sized for
 constexpr uint64_t BLOCK_RECORDS = 1u << 18;   // records per count-matrix row
@@ -63,7 +66,7 @@ int env_int(const char* name, int dflt) {
 }
 
 // Local-sort capacity per record width (SMEM ~ CAP*(kb+vb+2) bytes).
-inline int local_cap(int kb, int vb) { return (kb + vb) <= 8 ? 8192 : 4096; }
+inline int local_cap(int, int) { return LOCAL_NT * LOCAL_IPT; }
 
 // ---------------------------------------------------------------------------
 // Pinned host staging (grown on demand at sync points)
@@ -299,7 +302,6 @@ struct Sorter {
     Span* dsp = (Span*)meta.take(std::min<size_t>(spans.size(), SPAN_BATCH) * sizeof(Span) + 16);
     CopyR* dcp = (CopyR*)meta.take(std::min<size_t>(copies.size(), SPAN_BATCH) * sizeof(CopyR) + 16);
     if (!dsp || !dcp) return fail(DTS_ENOMEM, "workspace too small for span descriptors");
-    const int lcap = cap;
     for (size_t s0 = 0; s0 < spans.size(); s0 += SPAN_BATCH) {
       const size_t cnt = std::min<size_t>(SPAN_BATCH, spans.size() - s0);
       CUDA_TRY(cudaMemcpyAsync(dsp, hp + s0 * sizeof(Span), cnt * sizeof(Span),
@@ -308,18 +310,11 @@ struct Sorter {
       for (size_t i = s0; i < s0 + cnt; ++i) recs += spans[i].len;
       Timer::Ev ev;
       tm.begin(DTS_K_LOCAL, ev);
-      if (lcap == 8192) {
-        constexpr int C = 8192, NT = 512;
-        auto fn = k_local_sort<K, VB, NT, C>;
-        const size_t sm = local_layout(C, NT / 32, sizeof(K), VB).total;
+      {
+        auto fn = k_local_sort<K, VB, LOCAL_NT, LOCAL_IPT, LOCAL_RB>;
+        const size_t sm = local_layout(LOCAL_NT * LOCAL_IPT, LOCAL_NT, sizeof(K), VB, LOCAL_RB).total;
         DTS_TRY(set_smem(fn, sm));
-        fn<<<(unsigned)cnt, NT, sm, st>>>(dsp, Ak, Av, Tk, Tv);
-      } else {
-        constexpr int C = 4096, NT = 256;
-        auto fn = k_local_sort<K, VB, NT, C>;
-        const size_t sm = local_layout(C, NT / 32, sizeof(K), VB).total;
-        DTS_TRY(set_smem(fn, sm));
-        fn<<<(unsigned)cnt, NT, sm, st>>>(dsp, Ak, Av, Tk, Tv);
+        fn<<<(unsigned)cnt, LOCAL_NT, sm, st>>>(dsp, Ak, Av, Tk, Tv);
       }
       tm.end(ev, recs);
       DTS_TRY(check_launch("k_local_sort"));
@@ -494,7 +489,7 @@ struct Sorter {
       Timer::Ev ev;
       tm.begin(DTS_K_SCATTER, ev);
       auto fn = k_scatter<K, VB, SCAT_NT, SCAT_IPT, false>;
-      const size_t sm = scatter_layout(SCAT_TILE, SCAT_NT / 32, sizeof(K), VB, caps, false).total;
+      const size_t sm = scatter_layout(SCAT_TILE, SCAT_NT, sizeof(K), VB, caps, false).total;
       DTS_TRY(set_smem(fn, sm));
       const int grid = persistent_grid(fn, SCAT_NT, sm, (uint32_t)blks.size());
       fn<<<grid, SCAT_NT, sm, st>>>(dplans, dblks, (uint32_t)blks.size(), dctr + 1, ink, inv,
@@ -624,8 +619,6 @@ int sort_impl(void* keys, void* vals, uint64_t n, void* ws, size_t wsb, const dt
   S.rep = rep;
   S.st = st;
   S.cap = local_cap(sizeof(K), VB);
-  const int cap_env = env_int("DTS_LOCAL_CAP", 0);
-  if (cap_env == 4096 || cap_env == 8192) S.cap = cap_env;
   // theta: SortConfig.effective_theta (core.py:148-151), capped by SMEM.
   uint64_t theta = cfg->base_case_threshold;
   uint32_t gcap = std::min<uint32_t>((uint32_t)std::max(1, cfg->gamma_hi),
@@ -733,7 +726,7 @@ int partition_impl(const void* keys, const void* vals, uint64_t n, uint64_t gbas
   DTS_TRY(check_launch("k_bucket_bounds(split)"));
   {
     auto fn = k_scatter<K, VB, SCAT_NT, SCAT_IPT, true>;
-    const size_t sm = scatter_layout(SCAT_TILE, SCAT_NT / 32, sizeof(K), VB, caps, true).total;
+    const size_t sm = scatter_layout(SCAT_TILE, SCAT_NT, sizeof(K), VB, caps, true).total;
     DTS_TRY(set_smem(fn, sm));
     const int grid = persistent_grid(fn, SCAT_NT, sm, (uint32_t)blks.size());
     fn<<<grid, SCAT_NT, sm, st>>>(dplan, dblks, (uint32_t)blks.size(), dctr + 1, (const K*)keys,

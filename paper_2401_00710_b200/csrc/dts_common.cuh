@@ -113,6 +113,46 @@ __device__ __forceinline__ uint32_t peer_mask(uint32_t b, uint32_t valid_mask,
 #endif
 }
 
+// ---------------------------------------------------------------------------
+// Streaming loads / L2-sticky stores.  DTS_HINTS: 0 plain, 1 evict-first
+// loads, 2 evict-first loads + evict-last stores (keeps partially written
+// output lines in L2 until the next tile completes them).
+// ---------------------------------------------------------------------------
+#ifndef DTS_HINTS
+#define DTS_HINTS 0
+#endif
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) {
+#if DTS_HINTS >= 1
+  return __ldcs(p);
+#else
+  return *p;
+#endif
+}
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t pol = 0;
+#if DTS_HINTS >= 2
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
+  return pol;
+}
+__device__ __forceinline__ void st_keep(uint32_t* p, uint32_t v, uint64_t pol) {
+#if DTS_HINTS >= 2
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+#else
+  (void)pol;
+  *p = v;
+#endif
+}
+__device__ __forceinline__ void st_keep(uint64_t* p, uint64_t v, uint64_t pol) {
+#if DTS_HINTS >= 2
+  asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+#else
+  (void)pol;
+  *p = v;
+#endif
+}
+
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;
   x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -164,6 +204,97 @@ struct SplitRouter {
     return lo;
   }
 };
+
+// Block-wide exclusive scan of per-thread values (returns this thread's
+// exclusive prefix; *total receives the block total).  tmp: NT/32+1 words.
+template <int NT>
+__device__ __forceinline__ uint32_t block_exscan_val(uint32_t v, uint32_t* tmp, uint32_t* total) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) tmp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t w = lane < NW ? tmp[lane] : 0u;
+    uint32_t incl = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane < NW) tmp[lane] = incl - w;
+    if (lane == NW - 1) tmp[NW] = incl;
+  }
+  __syncthreads();
+  const uint32_t r = tmp[warp] + x - v;
+  *total = tmp[NW];
+  return r;
+}
+
+// Stable block radix rank with per-thread digit counters (counters laid
+// out [digit][thread] as u16, so a thread only touches its own column while
+// counting and the digit-major scan reproduces blocked input order).  Items
+// are in BLOCKED order: thread t owns positions t*IPT .. t*IPT+IPT-1.
+// `D` = number of digit values this pass (power of two, <= DMAX);
+// rank[i] receives the item's stable position in [0, NT*IPT).
+template <int NT, int IPT>
+__device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], const int D,
+                                           uint32_t (&rank)[IPT], uint16_t* cnt,
+                                           uint32_t* tmp) {
+  const int t = threadIdx.x;
+  for (int d = 0; d < D; ++d) cnt[d * NT + t] = 0;
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    uint16_t* c = cnt + dig[i] * NT + t;
+    const uint32_t o = *c;
+    rank[i] = o;
+    *c = (uint16_t)(o + 1);
+  }
+  __syncthreads();
+  // raking exclusive scan over the D*NT counters in [digit][thread] order;
+  // thread t owns counters [t*D, t*D + D)
+  uint16_t* mine = cnt + t * D;
+  uint32_t sum = 0;
+  if (D >= 8) {
+    for (int k = 0; k < D; k += 8) {
+      const uint4 q = *reinterpret_cast<const uint4*>(mine + k);
+      sum += (q.x & 0xffffu) + (q.x >> 16) + (q.y & 0xffffu) + (q.y >> 16) + (q.z & 0xffffu) +
+             (q.z >> 16) + (q.w & 0xffffu) + (q.w >> 16);
+    }
+  } else {
+    for (int k = 0; k < D; ++k) sum += mine[k];
+  }
+  uint32_t total;
+  uint32_t run = block_exscan_val<NT>(sum, tmp, &total);
+  if (D >= 8) {
+    for (int k = 0; k < D; k += 8) {
+      uint4 q = *reinterpret_cast<const uint4*>(mine + k);
+      uint32_t* w = reinterpret_cast<uint32_t*>(&q);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const uint32_t lo = w[h] & 0xffffu, hi = w[h] >> 16;
+        const uint32_t a = run, b = run + lo;
+        run = b + hi;
+        w[h] = (a & 0xffffu) | (b << 16);
+      }
+      *reinterpret_cast<uint4*>(mine + k) = q;
+    }
+  } else {
+    for (int k = 0; k < D; ++k) {
+      const uint32_t v = mine[k];
+      mine[k] = (uint16_t)run;
+      run += v;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) rank[i] += cnt[dig[i] * NT + t];
+}
 
 // Block-wide exclusive scan of a[0..n) in shared memory (in place); returns
 // the total.  All threads of the block must call it.  `tmp` holds NT/32

@@ -35,39 +35,6 @@ __host__ __device__ inline HistLayout hist_layout(int kb, Caps c, bool split) {
   return L;
 }
 
-struct ScatterLayout {
-  size_t run, sk, sv, hk, si, tst, hz, wh, sb, total;
-};
-__host__ __device__ inline ScatterLayout scatter_layout(int T, int NW, int kb, int vb,
-                                                        Caps c, bool split) {
-  ScatterLayout L;
-  size_t o = 0;
-  L.run = o; o = align16(o + (size_t)c.nbc * 8);
-  L.sk = o; o = align16(o + (size_t)T * kb);
-  L.sv = o; o = align16(o + (size_t)T * vb);
-  L.hk = o; o = align16(o + (size_t)c.hkc * kb);
-  L.si = o; o = align16(o + (split ? (size_t)c.hkc * 8 : 0));
-  L.tst = o; o = align16(o + ((size_t)c.nbc + 1) * 4);
-  L.hz = o; o = align16(o + (size_t)c.hzc * 4);
-  L.wh = o; o = align16(o + (size_t)NW * c.nbc * 2);
-  L.sb = o; o = align16(o + (size_t)T * 2);
-  L.total = o;
-  return L;
-}
-
-struct LocalLayout {
-  size_t sk, sv, si, wh, total;
-};
-__host__ __device__ inline LocalLayout local_layout(int CAP, int NW, int kb, int vb) {
-  LocalLayout L;
-  size_t o = 0;
-  L.sk = o; o = align16(o + (size_t)CAP * kb);
-  L.sv = o; o = align16(o + (size_t)CAP * vb);
-  L.si = o; o = align16(o + (size_t)CAP * 2);
-  L.wh = o; o = align16(o + (size_t)256 * NW * 2);
-  L.total = o;
-  return L;
-}
 
 // Load a segment's routing tables into shared memory.
 template <typename K>
@@ -241,95 +208,6 @@ __global__ void __launch_bounds__(NT) k_sample_plan(SegPlan* __restrict__ plans,
 }
 
 // ---------------------------------------------------------------------------
-// k_histogram: persistent CTAs pull blocks; per block, count records per
-// bucket in SMEM with warp-aggregated atomics (one atomic per distinct
-// bucket per warp step) and store the row into the [bucket][row] matrix.
-// counting.py:123-137.
-// ---------------------------------------------------------------------------
-template <typename K, int NT, bool SPLIT>
-__global__ void __launch_bounds__(NT) k_histogram(const SegPlan* __restrict__ plans,
-                                                  const Blk* __restrict__ blks, uint32_t nblk,
-                                                  uint32_t* __restrict__ ctr,
-                                                  const K* __restrict__ keys,
-                                                  uint32_t* __restrict__ counts,
-                                                  const K* __restrict__ heavy_pool,
-                                                  const uint32_t* __restrict__ hz_pool,
-                                                  const uint64_t* __restrict__ split_idx,
-                                                  uint64_t global_base, Caps caps) {
-  constexpr int VEC = 16 / sizeof(K);
-  constexpr int U = 4;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const HistLayout L = hist_layout(sizeof(K), caps, SPLIT);
-  K* hk = reinterpret_cast<K*>(smem_raw + L.hk);
-  uint64_t* si = reinterpret_cast<uint64_t*>(smem_raw + L.si);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw + L.hist);
-  uint32_t* hz = reinterpret_cast<uint32_t*>(smem_raw + L.hz);
-  __shared__ uint32_t s_blk;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-  for (;;) {
-    if (tid == 0) s_blk = atomicAdd(ctr, 1u);
-    __syncthreads();
-    const uint32_t bi = s_blk;
-    if (bi >= nblk) break;
-    const Blk B = blks[bi];
-    const SegPlan P = plans[B.seg];
-    for (uint32_t i = tid; i < P.nbmax; i += NT) hist[i] = 0;
-    load_tables<K>(P, heavy_pool, hz_pool, split_idx, hk, si, hz);
-    __syncthreads();
-    const Router<K> R = make_router<K>(P, hz, hk);
-    SplitRouter<K> SR;
-    SR.sk = hk; SR.si = si; SR.ns = P.nheavy;
-    const int nbits = max(1, (int)ceil_log2_u64(P.nb));
-
-    auto count_one = [&](K key, bool valid, uint64_t gidx) {
-      uint32_t b = 0;
-      if (valid) b = SPLIT ? SR(key, gidx) : R(key);
-      const uint32_t vm = __ballot_sync(FULL, valid);
-      if (vm == 0) return;
-      const uint32_t peers = peer_mask(b, vm, nbits);
-      if (valid && (peers & lanemask_lt()) == 0) atomicAdd(&hist[b], (uint32_t)__popc(peers));
-    };
-
-    const K* p = keys + B.begin;
-    const uint64_t n = B.end - B.begin;
-    const uint64_t addr = reinterpret_cast<uint64_t>(p);
-    uint64_t head = ((16 - (addr & 15)) & 15) / sizeof(K);
-    if (head > n) head = n;
-    const uint64_t nvec = (n - head) / VEC;
-    const uint64_t tail0 = head + nvec * VEC;
-    if (warp == 0) {
-      const uint64_t ntail = n - tail0;
-      uint64_t e = lane < head ? (uint64_t)lane : tail0 + (lane - head);
-      const bool valid = (uint64_t)lane < head + ntail;
-      count_one(valid ? p[e] : (K)0, valid, global_base + B.begin + e);
-    }
-    const uint4* pv = reinterpret_cast<const uint4*>(p + head);
-    for (uint64_t vb = 0; vb < nvec; vb += (uint64_t)NT * U) {
-      uint4 v[U];
-      bool ok[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint64_t vi = vb + (uint64_t)u * NT + tid;
-        ok[u] = vi < nvec;
-        if (ok[u]) v[u] = __ldg(pv + vi);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint64_t e0 = head + (vb + (uint64_t)u * NT + tid) * VEC;
-        const K* kk = reinterpret_cast<const K*>(&v[u]);
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) count_one(ok[u] ? kk[e] : (K)0, ok[u], global_base + B.begin + e0 + e);
-      }
-    }
-    __syncthreads();
-    uint32_t* row = counts + P.cnt_base + B.row;
-    for (uint32_t b = tid; b < P.nbmax; b += NT) row[(uint64_t)b * P.nrows] = hist[b];
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Flat exclusive scan u32 -> u64 (reduce / spine / downsweep).
 // ---------------------------------------------------------------------------
 constexpr int SCAN_NT = 256;
@@ -475,264 +353,6 @@ __global__ void __launch_bounds__(256) k_bucket_bounds(const SegPlan* __restrict
     }
     bstart[P.bs_base + b] = v;
     kinds[P.bs_base + b] = kind;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// k_scatter: persistent CTAs pull blocks; each block walks its tiles in
-// order.  Per tile: records go to registers (warp-contiguous, lane-striped,
-// i.e. input order), get a stable in-tile rank from warp-private counters and
-// ballot peer sets, are regrouped by bucket in SMEM, and are written out as
-// contiguous runs at run[b] (the block's running offset row — the GPU twin of
-// scatter_block's `run`, _kernels.py:19-25).  Stable for every block count.
-// ---------------------------------------------------------------------------
-template <typename K, int VB, int NT, int IPT, bool SPLIT>
-__global__ void __launch_bounds__(NT) k_scatter(const SegPlan* __restrict__ plans,
-                                                const Blk* __restrict__ blks, uint32_t nblk,
-                                                uint32_t* __restrict__ ctr,
-                                                const K* __restrict__ kin,
-                                                const typename ValOf<VB>::T* __restrict__ vin,
-                                                K* __restrict__ kout,
-                                                typename ValOf<VB>::T* __restrict__ vout,
-                                                const uint64_t* __restrict__ scan,
-                                                const K* __restrict__ heavy_pool,
-                                                const uint32_t* __restrict__ hz_pool,
-                                                const uint64_t* __restrict__ split_idx,
-                                                uint64_t global_base, Caps caps) {
-  using V = typename ValOf<VB>::T;
-  constexpr int NW = NT / 32;
-  constexpr int T = NT * IPT;
-  constexpr int IPW = 32 * IPT;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const ScatterLayout L = scatter_layout(T, NW, sizeof(K), VB, caps, SPLIT);
-  uint64_t* run = reinterpret_cast<uint64_t*>(smem_raw + L.run);
-  K* sk = reinterpret_cast<K*>(smem_raw + L.sk);
-  V* sv = reinterpret_cast<V*>(smem_raw + L.sv);
-  K* hk = reinterpret_cast<K*>(smem_raw + L.hk);
-  uint64_t* si = reinterpret_cast<uint64_t*>(smem_raw + L.si);
-  uint32_t* tst = reinterpret_cast<uint32_t*>(smem_raw + L.tst);
-  uint32_t* hz = reinterpret_cast<uint32_t*>(smem_raw + L.hz);
-  uint16_t* wh = reinterpret_cast<uint16_t*>(smem_raw + L.wh);
-  uint16_t* sb = reinterpret_cast<uint16_t*>(smem_raw + L.sb);
-  __shared__ uint32_t s_blk;
-  __shared__ uint32_t s_tmp[NW + 1];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t nbc = caps.nbc;
-  uint16_t* mywh = wh + warp * nbc;
-
-  for (;;) {
-    if (tid == 0) s_blk = atomicAdd(ctr, 1u);
-    __syncthreads();
-    const uint32_t bi = s_blk;
-    if (bi >= nblk) break;
-    const Blk B = blks[bi];
-    const SegPlan P = plans[B.seg];
-    const uint32_t nb = P.nb;
-    load_tables<K>(P, heavy_pool, hz_pool, split_idx, hk, si, hz);
-    {
-      const uint64_t* col = scan + P.cnt_base + B.row;
-      const uint64_t rb = P.offset - P.scanbase;
-      for (uint32_t b = tid; b < nb; b += NT) run[b] = rb + col[(uint64_t)b * P.nrows];
-      uint32_t* wh32 = reinterpret_cast<uint32_t*>(wh);
-      for (uint32_t i = tid; i < NW * nbc / 2; i += NT) wh32[i] = 0u;
-    }
-    __syncthreads();
-    const Router<K> R = make_router<K>(P, hz, hk);
-    SplitRouter<K> SR;
-    SR.sk = hk; SR.si = si; SR.ns = P.nheavy;
-    const int nbits = max(1, (int)ceil_log2_u64(nb));
-
-    for (uint64_t tile = B.begin; tile < B.end; tile += T) {
-      const uint64_t rem_ = B.end - tile;
-      const uint32_t tn = rem_ < (uint64_t)T ? (uint32_t)rem_ : (uint32_t)T;
-      K k[IPT];
-      V v[IPT];
-      uint32_t br[IPT];
-#pragma unroll
-      for (int j = 0; j < IPT; ++j) {
-        const uint32_t loc = warp * IPW + j * 32 + lane;
-        if (loc < tn) {
-          k[j] = kin[tile + loc];
-          if (VB) v[j] = vin[tile + loc];
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < IPT; ++j) {
-        const uint32_t loc = warp * IPW + j * 32 + lane;
-        const bool valid = loc < tn;
-        const uint32_t vm = __ballot_sync(FULL, valid);
-        br[j] = 0;
-        if (vm) {
-          uint32_t b = 0;
-          if (valid) b = SPLIT ? SR(k[j], global_base + tile + loc) : R(k[j]);
-          const uint32_t peers = peer_mask(b, vm, nbits);
-          const uint32_t before = __popc(peers & lanemask_lt());
-          uint32_t old = 0;
-          if (valid) old = mywh[b];
-          __syncwarp();
-          if (valid && before == 0) mywh[b] = (uint16_t)(old + __popc(peers));
-          __syncwarp();
-          br[j] = (b << 16) | (old + before);
-        }
-      }
-      __syncthreads();
-      // per bucket: exclusive prefix over warps (in place) and tile count
-      for (uint32_t b = tid; b < nb; b += NT) {
-        uint32_t s = 0;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-          const uint32_t t = wh[w * nbc + b];
-          wh[w * nbc + b] = (uint16_t)s;
-          s += t;
-        }
-        tst[b] = s;
-      }
-      __syncthreads();
-      block_exscan<NT>(tst, (int)nb, s_tmp);
-      if (tid == 0) tst[nb] = tn;
-      __syncthreads();
-#pragma unroll
-      for (int j = 0; j < IPT; ++j) {
-        const uint32_t loc = warp * IPW + j * 32 + lane;
-        if (loc < tn) {
-          const uint32_t b = br[j] >> 16;
-          const uint32_t pos = tst[b] + mywh[b] + (br[j] & 0xffffu);
-          sk[pos] = k[j];
-          if (VB) sv[pos] = v[j];
-          sb[pos] = (uint16_t)b;
-        }
-      }
-      __syncthreads();
-      for (uint32_t p = tid; p < tn; p += NT) {
-        const uint32_t b = sb[p];
-        const uint64_t d = run[b] + (p - tst[b]);
-        kout[d] = sk[p];
-        if (VB) vout[d] = sv[p];
-      }
-      __syncthreads();
-      for (uint32_t b = tid; b < nb; b += NT) run[b] += tst[b + 1] - tst[b];
-      {
-        uint32_t* wh32 = reinterpret_cast<uint32_t*>(wh);
-        for (uint32_t i = tid; i < NW * nbc / 2; i += NT) wh32[i] = 0u;
-      }
-      __syncthreads();
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// k_local_sort: one CTA per base-case span (<= CAP records).  Loads the span
-// into SMEM, finds the bits that differ inside it, and runs stable LSD passes
-// of <= 8 bits on (key, slot) pairs; payloads are gathered once at the end.
-// Output always lands in A.  dtsort.py:127-147 (stable sort by full key of a
-// span of adjacent buckets, valid per :128-131).
-// ---------------------------------------------------------------------------
-template <typename K, int VB, int NT, int CAP>
-__global__ void __launch_bounds__(NT) k_local_sort(const Span* __restrict__ spans,
-                                                   K* __restrict__ Ak,
-                                                   typename ValOf<VB>::T* __restrict__ Av,
-                                                   const K* __restrict__ Tk,
-                                                   const typename ValOf<VB>::T* __restrict__ Tv) {
-  using V = typename ValOf<VB>::T;
-  constexpr int W = sizeof(K) * 8;
-  constexpr int NW = NT / 32;
-  constexpr int IPT = CAP / NT;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const LocalLayout L = local_layout(CAP, NW, sizeof(K), VB);
-  K* sk = reinterpret_cast<K*>(smem_raw + L.sk);
-  V* sv = reinterpret_cast<V*>(smem_raw + L.sv);
-  uint16_t* si = reinterpret_cast<uint16_t*>(smem_raw + L.si);
-  uint16_t* wh = reinterpret_cast<uint16_t*>(smem_raw + L.wh);  // [digit][warp]
-  __shared__ uint32_t s_tmp[NW + 1];
-  __shared__ K s_diff[NW];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-  const Span S = spans[blockIdx.x];
-  const uint32_t n = S.len;
-  const K* srck = S.src ? Tk : Ak;
-  const V* srcv = S.src ? Tv : Av;
-  const K* gk = srck + S.offset;
-  const K k0 = gk[0];
-  K diff = 0;
-  for (uint32_t i = tid; i < n; i += NT) {
-    const K x = gk[i];
-    sk[i] = x;
-    diff |= x ^ k0;
-    if (VB) sv[i] = srcv[S.offset + i];
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) diff |= __shfl_xor_sync(FULL, diff, o);
-  if (lane == 0) s_diff[warp] = diff;
-  __syncthreads();
-  diff = 0;
-#pragma unroll
-  for (int w = 0; w < NW; ++w) diff |= s_diff[w];
-  int bits = 0;
-  if (diff) bits = (sizeof(K) == 8) ? 64 - __clzll((long long)diff) : 32 - __clz((int)(uint32_t)diff);
-
-  if (bits > 0) {
-    const int passes = (bits + 7) / 8;
-    const int R = (bits + passes - 1) / passes;
-    const uint32_t nd = 1u << R;
-    const uint32_t dmask = nd - 1u;
-    for (uint32_t i = tid; i < n; i += NT) si[i] = (uint16_t)i;
-    const uint32_t per = (((n + NW - 1) / NW) + 31u) & ~31u;  // items per warp
-    const uint32_t w0 = warp * per;
-    const uint32_t w1 = min(n, w0 + per);
-    for (int pass = 0; pass < passes; ++pass) {
-      const int shift = pass * R;
-      for (uint32_t i = tid; i < nd * NW; i += NT) wh[i] = 0;
-      __syncthreads();
-      K k[IPT];
-      uint32_t ix[IPT];
-      uint32_t br[IPT];
-#pragma unroll
-      for (int j = 0; j < IPT; ++j) {
-        const uint32_t loc = w0 + j * 32 + lane;
-        const bool valid = loc < w1;
-        br[j] = 0;
-        if ((uint32_t)(j * 32) >= per) continue;  // warp-uniform
-        if (valid) {
-          k[j] = sk[loc];
-          ix[j] = si[loc];
-        }
-        const uint32_t vm = __ballot_sync(FULL, valid);
-        if (!vm) continue;
-        const uint32_t d = valid ? (uint32_t)(k[j] >> shift) & dmask : 0u;
-        const uint32_t peers = peer_mask(d, vm, R);
-        const uint32_t before = __popc(peers & lanemask_lt());
-        uint32_t old = 0;
-        if (valid) old = wh[d * NW + warp];
-        __syncwarp();
-        if (valid && before == 0) wh[d * NW + warp] = (uint16_t)(old + __popc(peers));
-        __syncwarp();
-        br[j] = (d << 16) | (old + before);
-      }
-      __syncthreads();
-      block_exscan<NT>(wh, (int)(nd * NW), s_tmp);
-#pragma unroll
-      for (int j = 0; j < IPT; ++j) {
-        const uint32_t loc = w0 + j * 32 + lane;
-        if ((uint32_t)(j * 32) < per && loc < w1) {
-          const uint32_t d = br[j] >> 16;
-          const uint32_t pos = wh[d * NW + warp] + (br[j] & 0xffffu);
-          sk[pos] = k[j];
-          si[pos] = (uint16_t)ix[j];
-        }
-      }
-      __syncthreads();
-    }
-    K* ok = Ak + S.offset;
-    for (uint32_t i = tid; i < n; i += NT) {
-      ok[i] = sk[i];
-      if (VB) Av[S.offset + i] = sv[si[i]];
-    }
-  } else if (S.src) {
-    K* ok = Ak + S.offset;
-    for (uint32_t i = tid; i < n; i += NT) {
-      ok[i] = sk[i];
-      if (VB) Av[S.offset + i] = sv[i];
-    }
   }
 }
 
