@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark: DovetailSort of BASELINE.json's headline configuration on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2|c1|c3-zipf1.0|c4-exp1e-5|...] [--n N]
+
+Default workload (BASELINE.json configs[1], "C2"): 10^9 records of uint32
+key + uint32 value, keys i.i.d. uniform on [0, 10^9) from a seeded torch
+generator, values = original index.  A step = one full stable sort of that
+batch, device-resident when the timed region starts (the per-step restore
+of the unsorted input is outside the CUDA-event bracket).  Inputs (8 GB)
+exceed the 126 MB L2, so no flush is needed between steps.
+
+--impl reference times the reference algorithm's CPU implementation on the
+host cores (the C++ oracle restatement, oracle/; the reference itself is
+Python and cannot travel to the GPU box) on a bounded sample of the same
+workload.  Prints one JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gkeys/s sorted (32/64-bit key-value) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "Gkeys/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+CONFIGS = {
+    "c1": dict(desc="C1 keys-only u32 uniform [0,2^32), n=1e6", n=10**6, kb=4, vb=0, dist="u32full"),
+    "c2": dict(desc="C2 u32 key + u32 value, keys uniform [0,1e9), values = index, n=1e9",
+               n=10**9, kb=4, vb=4, dist="uniform1e9"),
+    "c3-zipf0.6": dict(desc="C3 Zipf s=0.6 ranks over 1..1e9 mapped by a seeded permutation",
+                       n=10**9, kb=4, vb=4, dist="zipf", s=0.6),
+    "c3-zipf1.0": dict(desc="C3 Zipf s=1.0", n=10**9, kb=4, vb=4, dist="zipf", s=1.0),
+    "c3-zipf1.2": dict(desc="C3 Zipf s=1.2", n=10**9, kb=4, vb=4, dist="zipf", s=1.2),
+    "c3-zipf1.5": dict(desc="C3 Zipf s=1.5", n=10**9, kb=4, vb=4, dist="zipf", s=1.5),
+    "c4-exp1e-5": dict(desc="C4 u64/u64 keys floor(Exp(rate 1e-5))", n=10**9, kb=8, vb=8,
+                       dist="exp", rate=1e-5),
+    "c4-exp1e-7": dict(desc="C4 u64/u64 keys floor(Exp(rate 1e-7))", n=10**9, kb=8, vb=8,
+                       dist="exp", rate=1e-7),
+    "c4-bexp": dict(desc="C4 u64/u64 keys w >> Geometric(0.5)", n=10**9, kb=8, vb=8, dist="bexp"),
+}
+
+
+def gen_device(cfg, n, seed, device, gbase=0):
+    """Seeded synthetic keys on the GPU (see gen.py for the distributions)."""
+    from paper_2401_00710_b200 import gen
+
+    return gen.generate_device(cfg, n, seed, device, gbase)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle restatement on host cores
+# ---------------------------------------------------------------------------
+def cpu_sample_sort(cfgd, n, seed, threads=0):
+    from oracle import oracle as ora
+
+    keys, vals = gen_host(cfgd, n, seed)
+    t0 = time.perf_counter()
+    ora.sort_inplace(keys, vals, "dt", threads=threads)
+    dt = time.perf_counter() - t0
+    return dt, keys, vals
+
+
+def gen_host(cfgd, n, seed):
+    rng = np.random.default_rng(seed)
+    d = cfgd["dist"]
+    if d == "uniform1e9":
+        k = rng.integers(0, 10**9, size=n, dtype=np.uint32)
+    elif d == "u32full":
+        k = rng.integers(0, 2**32, size=n, dtype=np.uint32)
+    elif d == "exp":
+        k = np.floor(rng.exponential(1.0 / cfgd["rate"], size=n)).astype(np.uint64)
+    elif d == "bexp":
+        w = rng.integers(0, 2**64 - 1, size=n, dtype=np.uint64, endpoint=True)
+        g = np.minimum(rng.geometric(0.5, size=n) - 1, 63).astype(np.uint64)
+        k = w >> g
+    elif d == "zipf":
+        from paper_2401_00710_b200 import gen
+
+        k = gen.zipf_keys_host(cfgd["s"], n, 10**9, seed)
+    else:
+        raise ValueError(d)
+    vdt = {0: None, 4: np.uint32, 8: np.uint64}[cfgd["vb"]]
+    v = None if vdt is None else np.arange(n, dtype=vdt)
+    return k, v
+
+
+def cpu_bounded_sample(cfgd, seed, budget_s=12.0, n0=10**7, nmax=None):
+    """Sort growing samples until one run takes >= budget/2 seconds."""
+    nmax = nmax or cfgd["n"]
+    n = min(n0, nmax)
+    dt = 0.0
+    while True:
+        dt, _, _ = cpu_sample_sort(cfgd, n, seed)
+        if dt >= budget_s / 2 or n >= nmax:
+            break
+        n = min(nmax, n * 4 if dt < budget_s / 8 else n * 2)
+    return n, dt
+
+
+def run_reference(args, cfgd, rank, world):
+    if rank != 0:
+        return
+    from oracle import oracle as ora
+
+    cores = ora.max_threads()
+    n, _ = cpu_bounded_sample(cfgd, seed=1, budget_s=8.0)
+    times = []
+    for _ in range(args.warmup):
+        cpu_sample_sort(cfgd, n, 1)
+    for _ in range(args.steps):
+        dt, _, _ = cpu_sample_sort(cfgd, n, 1)
+        times.append(dt)
+    ms = 1e3 * float(np.mean(times))
+    value = n / (ms / 1e3) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32" if cfgd["kb"] == 4 else "u64", "data": "synthetic",
+        "config": {"workload": args.config, "desc": cfgd["desc"], "sample_records": n},
+        "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{n} records of the {args.config} workload, oracle dt_sort "
+                                   f"(C++ restatement of the reference, OpenMP {cores} threads)"},
+        "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, cfgd, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2401_00710_b200 import RecordArray, SortConfig, dt_sort
+    from paper_2401_00710_b200.dtsort import sort_device
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    n = args.n or cfgd["n"]
+    kb, vb = cfgd["kb"], cfgd["vb"]
+    cfg = SortConfig(seed=0)
+    src_k, src_v = gen_device(cfgd, n, 1000 + rank, dev, gbase=rank * n)
+    k = torch.empty_like(src_k)
+    v = None if src_v is None else torch.empty_like(src_v)
+    from paper_2401_00710_b200 import _lib
+
+    ws = torch.empty(int(_lib.lib().dts_workspace_bytes(n, kb, vb)), dtype=torch.uint8, device=dev)
+    multi = world > 1
+    if multi:
+        from paper_2401_00710_b200.distributed import CudaOps, dist_sort
+
+        ops = CudaOps(cfg)
+
+    def restore():
+        k.copy_(src_k)
+        if v is not None:
+            v.copy_(src_v)
+
+    def one_sort(profile=False):
+        if multi:
+            rk, rv, st = dist_sort(k, v, ops=ops)
+            return None, st
+        return sort_device(k, v, cfg, 0, profile=profile, workspace=ws, report=True), None
+
+    for _ in range(args.warmup):
+        restore()
+        one_sort()
+    torch.cuda.synchronize()
+    # correctness certificate on the last warm-up output (values = index)
+    if not multi and v is not None:
+        ok = bool((k[1:].to(torch.int64) & 0xFFFFFFFF >= (k[:-1].to(torch.int64) & 0xFFFFFFFF)).all()) \
+            if kb == 4 else True
+        if not ok:
+            raise SystemExit("sorted-order check failed")
+
+    clocks = Clocks(local_rank)
+    if multi:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    total_ms = 0.0
+    reps = []
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.steps):
+        restore()
+        torch.cuda.synchronize()
+        if multi:
+            dist.barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        rep, st = one_sort(profile=not multi)
+        b.record(stream)
+        b.synchronize()
+        total_ms += a.elapsed_time(b)
+        reps.append(rep)
+    torch.cuda.synchronize()
+    if multi:
+        dist.barrier()
+    clk = clocks.stop()
+    ms_local = total_ms / args.steps
+    if multi:
+        t = torch.tensor([ms_local], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    else:
+        ms = ms_local
+    n_total = n * world
+    value = n_total / (ms / 1e3) / 1e9
+
+    # roofline of the dominant kernel (k_scatter), CUDA events inside the
+    # library on the launching stream, summed over the timed steps
+    peak, peak_kind = peaks()
+    roof = None
+    launches = None
+    if not multi and reps and reps[0] is not None:
+        sc_ms = sum(r.kernel_ms["scatter"] for r in reps)
+        sc_launch = sum(r.kernel_launches["scatter"] for r in reps)
+        sc_rec = sum(r.kernel_records["scatter"] for r in reps)
+        bytes_alg = sc_rec * 2 * (kb + vb)  # read + write of every record
+        per_launch_ms = sc_ms / max(sc_launch, 1)
+        per_launch_bytes = bytes_alg / max(sc_launch, 1)
+        achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
+        launches = int(sum(r.gpu_launches for r in reps))
+        shares = {c: round(sum(r.kernel_ms[c] for r in reps) / (ms * args.steps), 4)
+                  for c in reps[0].kernel_ms}
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                traffic = json.load(f).get("k_scatter_bytes_per_launch")
+        except Exception:
+            pass
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": "k_scatter", "peak_kind": peak_kind,
+                "algorithmic_bytes_per_launch": int(per_launch_bytes),
+                "ms_per_launch": round(per_launch_ms, 4),
+                "step_share": shares}
+        D_ref = 3 * n if args.config == "c2" else None
+        D_ours = reps[0].records_distributed
+        beta = kb + 2 * (kb + vb)
+        pipe = {"beta_bytes": beta, "D_ours": D_ours, "D_reference": D_ref,
+                "B_alg_GB": round(beta * (D_ref or D_ours) / 1e9, 3),
+                "achieved_GBps": round(beta * (D_ref or D_ours) / (ms / 1e3) / 1e9, 1),
+                "frac_of_peak": round(beta * (D_ref or D_ours) / (ms / 1e3) / 1e9 / peak, 4)}
+    else:
+        pipe = None
+
+    # end to end through the public API with pinned host buffers
+    e2e = None
+    if not multi and not args.no_e2e:
+        hk = torch.empty(n, dtype=src_k.dtype, pin_memory=True)
+        hv = None if src_v is None else torch.empty(n, dtype=src_v.dtype, pin_memory=True)
+        pristine_k = src_k.cpu()
+        pristine_v = None if src_v is None else src_v.cpu()
+        ku = hk.view(torch.uint32 if kb == 4 else torch.uint64)
+        vu = None if hv is None else hv.view(torch.uint32 if vb == 4 else torch.uint64)
+        e_steps = max(1, min(args.steps, args.e2e_steps))
+        e_ms = 0.0
+        for i in range(e_steps + 1):
+            hk.copy_(pristine_k)
+            if hv is not None:
+                hv.copy_(pristine_v)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dt_sort(RecordArray(ku, vu), cfg)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            if i > 0:
+                e_ms += (t1 - t0) * 1e3
+        e_ms /= e_steps
+        e2e = {"value": round(n / (e_ms / 1e3) / 1e9, 4), "unit": UNIT,
+               "h2d_bytes_per_step": n * (kb + vb), "d2h_bytes_per_step": n * (kb + vb),
+               "ms_per_step": round(e_ms, 2), "steps": e_steps,
+               "path": "dt_sort(RecordArray(pinned host tensors)) -> H2D, dts_sort, D2H"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle import oracle as ora
+
+        ns, dts = cpu_bounded_sample(cfgd, seed=1, budget_s=args.cpu_budget)
+        cpu = {"value": round(ns / dts / 1e9, 6), "unit": UNIT, "cores": ora.max_threads(),
+               "kind": "port",
+               "sample": f"{ns} records of the {args.config} workload sorted by the oracle "
+                         f"(C++ restatement of the reference dt_sort) in {dts:.2f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u32" if kb == 4 else "u64", "data": "synthetic (seeded torch generator on device)",
+            "config": {"workload": args.config, "desc": cfgd["desc"], "n_per_gpu": n,
+                       "key_bytes": kb, "val_bytes": vb, "parallelism": f"keyrange{world}" if multi else "single",
+                       "l2": "inputs (n*(k+v) bytes) exceed the 126 MB L2; no flush needed",
+                       "timed": "CUDA events around each sort; per-step input restore outside"},
+            "roofline": roof, "pipeline_roofline": pipe, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    cfgd = dict(CONFIGS[args.config])
+    if args.n:
+        cfgd["n"] = args.n
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfgd, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, cfgd, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

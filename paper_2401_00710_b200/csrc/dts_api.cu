@@ -46,9 +46,6 @@ int fail(int code, const std::string& msg) {
 // Tunables (B200-sized)
 // ---------------------------------------------------------------------------
 constexpr int HIST_NT = 512;
-constexpr int SCAT_NT = 256;
-constexpr int SCAT_IPT = 17;                   // odd: conflict-free blocked SMEM reads
-constexpr int SCAT_TILE = SCAT_NT * SCAT_IPT;  // 4352 records per tile
 constexpr int LOCAL_NT = 256;
 constexpr int LOCAL_IPT = 17;
 constexpr int LOCAL_RB = 5;                    // radix bits per local-sort pass
@@ -57,6 +54,7 @@ constexpr uint32_t GMAX_HW = 10;               // widest digit the scatter is si
 constexpr uint64_t BLOCK_RECORDS = 1u << 18;   // records per count-matrix row
 constexpr uint32_t COPY_CHUNK = 1u << 16;
 constexpr uint64_t SPAN_BATCH = 1u << 18;      // spans per k_local_sort launch
+constexpr uint64_t SAMPLE_FACTOR = 2;          // sample iff n' >= 2|S| (dtsort.py:225)
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -266,6 +264,20 @@ struct Sorter {
     return std::max<uint32_t>(g, 1);
   }
 
+  // dt_sort sampling decision (dtsort.py:225-228: sample only when the
+  // segment holds at least SAMPLE_FACTOR x the sample).  Adjusts g (<= 9)
+  // and returns the subsample exponent gs (|S| = 2^gs * stride).
+  bool sampled_plan(uint64_t len, uint32_t remaining, uint32_t& g, uint32_t& gs) const {
+    const uint32_t g9 = std::min<uint32_t>(g, 9);
+    gs = std::min<uint32_t>(g9 > 1 ? g9 - 1 : 1, gs_max);
+    uint64_t S = std::min<uint64_t>(len, (uint64_t(1) << gs) * stride);
+    S = std::min<uint64_t>(S, smax);
+    if (len < SAMPLE_FACTOR * S) return false;
+    g = std::min(g9, remaining);
+    gs = std::min<uint32_t>(gs, g > 1 ? g - 1 : 1);
+    return true;
+  }
+
   void flush_span() {
     if (have_cur && cur.len) spans.push_back(cur);
     have_cur = false;
@@ -353,13 +365,12 @@ struct Sorter {
     std::vector<uint32_t> sampled;
     uint64_t cnt_total = 0, bs_total = 0, heavy_total = 0, hz_total = 0, scanbase = 0;
     uint32_t nbc = 2, hzc = 0, hkc = 0;
-    bool any_heavy_possible = false;
     for (size_t i = 0; i < ns; ++i) {
       const HostSeg& hs = segs[s0 + i];
       SegPlan& P = plans[i];
       std::memset(&P, 0, sizeof(P));
       const uint32_t remaining = W - hs.consumed;
-      const uint32_t g = choose_gamma(hs.len, remaining);
+      uint32_t g = choose_gamma(hs.len, remaining);
       P.offset = hs.offset;
       P.len = hs.len;
       P.scanbase = scanbase;
@@ -369,27 +380,27 @@ struct Sorter {
       P.consumed = hs.consumed;
       P.nb = 1u << g;
       P.nbmax = P.nb;
-      if (dt) {
-        const uint32_t gs = std::min(g, gs_max);
-        uint64_t S = std::min<uint64_t>(hs.len, (uint64_t(1) << gs) * stride);
-        S = std::min<uint64_t>(S, smax);
-        if (hs.len >= 2 * S) {
-          P.flags |= PF_SAMPLE;
-          if (hs.root && hs.consumed == 0) P.flags |= PF_ROOTSKIP;
-          P.nbmax = (1u << g) + (1u << gs) + 1u;
-          P.heavy_base = (uint32_t)heavy_total;
-          heavy_total += (1u << gs);
-          P.hz_base = (uint32_t)hz_total;
-          hz_total += (1u << g) + 1u;
-          sampled.push_back((uint32_t)i);
-          any_heavy_possible = true;
-          hzc = std::max(hzc, (1u << g) + 1u);
-          hkc = std::max(hkc, 1u << gs);
-        }
+      uint32_t gs = 0;
+      if (dt && sampled_plan(hs.len, remaining, g, gs)) {
+        // sampled segments may gain heavy / overflow buckets; the digit is
+        // capped so bucket ids stay below the scatter's 2^10 capacity
+        P.gamma = g;
+        P.shift = remaining - g;
+        P.flags |= PF_SAMPLE;
+        P.sample_gs = gs;
+        if (hs.root && hs.consumed == 0) P.flags |= PF_ROOTSKIP;
+        P.nb = 1u << g;
+        P.nbmax = (1u << g) + (1u << gs) + 1u;
+        P.heavy_base = (uint32_t)heavy_total;
+        heavy_total += (1u << gs);
+        P.hz_base = (uint32_t)hz_total;
+        hz_total += (1u << g) + 1u;
+        sampled.push_back((uint32_t)i);
+        hzc = std::max(hzc, (1u << g) + 1u);
+        hkc = std::max(hkc, 1u << gs);
       }
       const uint64_t rows = std::max<uint64_t>(1, (hs.len + BLOCK_RECORDS - 1) / BLOCK_RECORDS);
       P.nrows = (uint32_t)rows;
-      P.row0 = (uint32_t)blks.size();
       P.cnt_base = cnt_total;
       cnt_total += (uint64_t)P.nbmax * rows;
       P.bs_base = (uint32_t)bs_total;
@@ -405,7 +416,6 @@ struct Sorter {
         blks.push_back(b);
       }
     }
-    (void)any_heavy_possible;
     nbc = (nbc + 1) & ~1u;
     Caps caps{nbc, hzc, hkc, 0};
 
@@ -488,11 +498,12 @@ struct Sorter {
       CUDA_TRY(cudaMemsetAsync(dctr + 1, 0, 4, st));
       Timer::Ev ev;
       tm.begin(DTS_K_SCATTER, ev);
-      auto fn = k_scatter<K, VB, SCAT_NT, SCAT_IPT, false>;
-      const size_t sm = scatter_layout(SCAT_TILE, SCAT_NT, sizeof(K), VB, caps, false).total;
+      using TL = ScatterTile<K, VB>;
+      auto fn = k_scatter<K, VB, false>;
+      const size_t sm = scatter_layout(TL::T, TL::NT, TL::A, sizeof(K), VB, caps, false).total;
       DTS_TRY(set_smem(fn, sm));
-      const int grid = persistent_grid(fn, SCAT_NT, sm, (uint32_t)blks.size());
-      fn<<<grid, SCAT_NT, sm, st>>>(dplans, dblks, (uint32_t)blks.size(), dctr + 1, ink, inv,
+      const int grid = persistent_grid(fn, TL::NT, sm, (uint32_t)blks.size());
+      fn<<<grid, TL::NT, sm, st>>>(dplans, dblks, (uint32_t)blks.size(), dctr + 1, ink, inv,
                                     outk, outv, dscan, dheavy, dhz, nullptr, 0, caps);
       tm.end(ev, wave_recs);
       DTS_TRY(check_launch("k_scatter"));
@@ -725,11 +736,12 @@ int partition_impl(const void* keys, const void* vals, uint64_t n, uint64_t gbas
   k_bucket_bounds<<<1, 256, 0, st>>>(dplan, dscan, nullptr, dbs, dkinds);
   DTS_TRY(check_launch("k_bucket_bounds(split)"));
   {
-    auto fn = k_scatter<K, VB, SCAT_NT, SCAT_IPT, true>;
-    const size_t sm = scatter_layout(SCAT_TILE, SCAT_NT, sizeof(K), VB, caps, true).total;
+    using TL = ScatterTile<K, VB>;
+    auto fn = k_scatter<K, VB, true>;
+    const size_t sm = scatter_layout(TL::T, TL::NT, TL::A, sizeof(K), VB, caps, true).total;
     DTS_TRY(set_smem(fn, sm));
-    const int grid = persistent_grid(fn, SCAT_NT, sm, (uint32_t)blks.size());
-    fn<<<grid, SCAT_NT, sm, st>>>(dplan, dblks, (uint32_t)blks.size(), dctr + 1, (const K*)keys,
+    const int grid = persistent_grid(fn, TL::NT, sm, (uint32_t)blks.size());
+    fn<<<grid, TL::NT, sm, st>>>(dplan, dblks, (uint32_t)blks.size(), dctr + 1, (const K*)keys,
                                   (const V*)vals, (K*)okeys, (V*)ovals, dscan, dsk, nullptr, dsi,
                                   gbase, caps);
     DTS_TRY(check_launch("k_scatter(split)"));

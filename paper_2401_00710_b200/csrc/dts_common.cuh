@@ -38,7 +38,7 @@ struct SegPlan {
   uint32_t heavy_base;
   uint32_t hz_base;   // zone table at hz_pool[hz_base .. +2^gamma]
   uint32_t flags;
-  uint32_t row0;      // first block row (unused by kernels, kept for debug)
+  uint32_t sample_gs; // sampled segments: |S| = 2^sample_gs * stride
   uint32_t nrows;     // block rows of this segment
   uint32_t consumed;  // top bits known equal across the segment
   uint32_t bs_base;   // bucket-bounds / kinds base index (nbmax+1 entries)
@@ -151,6 +151,44 @@ __device__ __forceinline__ void st_keep(uint64_t* p, uint64_t v, uint64_t pol) {
   (void)pol;
   *p = v;
 #endif
+}
+
+// ---------------------------------------------------------------------------
+// TMA 1-D bulk copies (cp.async.bulk) completed on an mbarrier.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(NT) k_sample_plan(SegPlan* __restrict__ plans,
 
   const uint32_t s = seg_ids[blockIdx.x];
   SegPlan P = plans[s];
-  const uint32_t gs = min(P.gamma, gs_max);
+  const uint32_t gs = min(P.sample_gs, gs_max);
   uint64_t S = (uint64_t(1) << gs) * stride;
   if (S > P.len) S = P.len;
   if (S > smax) S = smax;
@@ -176,7 +176,10 @@ __global__ void __launch_bounds__(NT) k_sample_plan(SegPlan* __restrict__ plans,
     if (f) hk_out[s_tmp[warp] + __popc(bal & lanemask_lt())] = v;
     __syncthreads();
   }
-  const uint32_t m = s_m;
+  // the host reserved nbmax = 2^gamma + 2^gs + 1 columns: keep 2m within it
+  // (dropping a heavy key only leaves it in its light bucket)
+  const uint32_t m_cap = (P.nbmax - (1u << gamma) - 1u) / 2u;
+  const uint32_t m = min(s_m, m_cap);
   __syncthreads();
   // copy heavy keys back into SMEM (sm is free now) for the zone table
   for (uint32_t i = threadIdx.x; i < m; i += NT) sm[i] = hk_out[i];

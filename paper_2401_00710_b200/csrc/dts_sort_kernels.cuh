@@ -125,65 +125,151 @@ __device__ __forceinline__ uint32_t stage_tile(T* buf, const T* __restrict__ src
   return off;
 }
 
-struct ScatterLayout {
-  size_t run, sk, sv, hk, si, pk, cnt, tst, hz, total;
+// Per-(key, value) width tiling of the scatter.
+template <typename K, int VB> struct ScatterTile {
+  static constexpr int NT = 512;
+  static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? 9 : 5;  // odd: conflict-free
+  static constexpr int T = NT * IPT;
+  static constexpr int AK = 32 / (int)sizeof(K);
+  static constexpr int AV = VB ? 32 / VB : AK;
+  static constexpr int A = AK > AV ? AK : AV;  // flush granularity (records): whole sectors
+  static constexpr int NBC = 1024;             // bucket capacity (ids < 2^10)
 };
-__host__ __device__ inline ScatterLayout scatter_layout(int T, int NT, int kb, int vb, Caps c,
-                                                        bool split) {
+
+struct ScatterLayout {
+  size_t run, sk, sv, lk, lv, hk, si, pk, cnt, tst, fl, loc, hz, bar, total;
+};
+__host__ __device__ inline ScatterLayout scatter_layout(int T, int NT, int A, int kb, int vb,
+                                                        Caps c, bool split) {
   ScatterLayout L;
   size_t o = 0;
-  L.run = o; o = align16(o + (size_t)c.nbc * 8);
-  L.sk = o; o = align16(o + (size_t)(T + 4) * kb);
-  L.sv = o; o = align16(o + (size_t)(T + 4) * vb);
+  const size_t nb = c.nbc;
+  L.run = o; o = align16(o + nb * 8);
+  L.sk = o; o = align16(o + 2 * (size_t)(T + 8) * kb);
+  L.sv = o; o = align16(o + 2 * (size_t)(T + 8) * vb);
+  L.lk = o; o = align16(o + nb * A * kb);
+  L.lv = o; o = align16(o + nb * A * vb);
   L.hk = o; o = align16(o + (size_t)c.hkc * kb);
   L.si = o; o = align16(o + (split ? (size_t)c.hkc * 8 : 0));
   L.pk = o; o = align16(o + (size_t)T * 4);
-  L.cnt = o; o = align16(o + (size_t)64 * NT * 2);
-  L.tst = o; o = align16(o + ((size_t)c.nbc + 1) * 4);
+  L.cnt = o; o = align16(o + (size_t)32 * NT * 2);
+  L.tst = o; o = align16(o + (nb + 1) * 4);
+  L.fl = o; o = align16(o + nb * 4);
+  L.loc = o; o = align16(o + nb);
   L.hz = o; o = align16(o + (size_t)c.hzc * 4);
+  L.bar = o; o = align16(o + 16);
   L.total = o;
   return L;
 }
 
+// Issue the TMA copy of tile [g0, g0+tn) of one column into `buf` (element e
+// at buf[off + e], off = g0 % VEC): the 16-byte aligned body goes through
+// cp.async.bulk on `bar`; returns the body bytes.  Head/tail elements (< VEC
+// each) are loaded by the caller.
+template <typename T>
+__device__ __forceinline__ uint32_t tile_body(uint64_t g0, uint32_t tn, uint32_t& off,
+                                              uint32_t& head, uint32_t& nbody) {
+  constexpr uint32_t VEC = 16 / sizeof(T);
+  off = (uint32_t)(g0 % VEC);
+  const uint32_t h0 = (VEC - off) % VEC;
+  head = h0 < tn ? h0 : tn;
+  nbody = ((tn - head) / VEC) * VEC;
+  return nbody * (uint32_t)sizeof(T);
+}
+
 // ---------------------------------------------------------------------------
-// k_scatter: persistent CTAs pull blocks; each block walks its tiles in
-// input order.  Per tile: stage keys/values in SMEM, route every record to
-// its bucket, count the tile histogram with SMEM atomics, then stably sort
-// the tile's (bucket, slot) words by bucket with 2 passes of a per-thread
-// counter block radix rank and write each bucket's run contiguously at
-// run[b] — the block's running offset row, the GPU twin of scatter_block's
-// `run` (_kernels.py:19-25).  Stable for every block count.
+// k_scatter: one persistent CTA per SM pulls blocks; each block walks its
+// tiles in input order.  Per tile:
+//   * the tile's keys/values arrive in SMEM by TMA bulk copy (the next tile
+//     is prefetched into the other buffer while this one is processed);
+//   * every record is routed to its bucket (tile histogram by SMEM atomics);
+//   * the tile's (bucket, slot) words are stably sorted by bucket with
+//     per-thread-counter block radix rank passes (<= 5 bits each);
+//   * bucket runs are written at run[b] — the block's running offset row,
+//     the GPU twin of scatter_block's `run` (_kernels.py:19-25) — through a
+//     per-bucket SMEM write-combining buffer so global stores only ever
+//     complete whole 32-byte sectors (no L2 partial-sector evictions).
+// Stable for every block count (counting.py:1-10 invariant).
 // ---------------------------------------------------------------------------
-template <typename K, int VB, int NT, int IPT, bool SPLIT>
-__global__ void __launch_bounds__(NT, 2) k_scatter(const SegPlan* __restrict__ plans,
-                                                const Blk* __restrict__ blks, uint32_t nblk,
-                                                uint32_t* __restrict__ ctr,
-                                                const K* __restrict__ kin,
-                                                const typename ValOf<VB>::T* __restrict__ vin,
-                                                K* __restrict__ kout,
-                                                typename ValOf<VB>::T* __restrict__ vout,
-                                                const uint64_t* __restrict__ scan,
-                                                const K* __restrict__ heavy_pool,
-                                                const uint32_t* __restrict__ hz_pool,
-                                                const uint64_t* __restrict__ split_idx,
-                                                uint64_t global_base, Caps caps) {
+template <typename K, int VB, bool SPLIT>
+__global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 1)
+    k_scatter(const SegPlan* __restrict__ plans, const Blk* __restrict__ blks, uint32_t nblk,
+              uint32_t* __restrict__ ctr, const K* __restrict__ kin,
+              const typename ValOf<VB>::T* __restrict__ vin, K* __restrict__ kout,
+              typename ValOf<VB>::T* __restrict__ vout, const uint64_t* __restrict__ scan,
+              const K* __restrict__ heavy_pool, const uint32_t* __restrict__ hz_pool,
+              const uint64_t* __restrict__ split_idx, uint64_t global_base, Caps caps) {
   using V = typename ValOf<VB>::T;
-  constexpr int T = NT * IPT;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const ScatterLayout L = scatter_layout(T, NT, sizeof(K), VB, caps, SPLIT);
+  using TL = ScatterTile<K, VB>;
+  constexpr int NT = TL::NT, IPT = TL::IPT, T = TL::T, A = TL::A;
+  constexpr uint64_t AM = A - 1;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const ScatterLayout L = scatter_layout(T, NT, A, sizeof(K), VB, caps, SPLIT);
   uint64_t* run = reinterpret_cast<uint64_t*>(smem_raw + L.run);
-  K* sk = reinterpret_cast<K*>(smem_raw + L.sk);
-  V* sv = reinterpret_cast<V*>(smem_raw + L.sv);
+  K* skb = reinterpret_cast<K*>(smem_raw + L.sk);
+  V* svb = reinterpret_cast<V*>(smem_raw + L.sv);
+  K* lk = reinterpret_cast<K*>(smem_raw + L.lk);
+  V* lv = reinterpret_cast<V*>(smem_raw + L.lv);
   K* hk = reinterpret_cast<K*>(smem_raw + L.hk);
   uint64_t* si = reinterpret_cast<uint64_t*>(smem_raw + L.si);
   uint32_t* pk = reinterpret_cast<uint32_t*>(smem_raw + L.pk);
   uint16_t* cnt = reinterpret_cast<uint16_t*>(smem_raw + L.cnt);
   uint32_t* tst = reinterpret_cast<uint32_t*>(smem_raw + L.tst);
+  int32_t* fl = reinterpret_cast<int32_t*>(smem_raw + L.fl);
+  uint8_t* loc = reinterpret_cast<uint8_t*>(smem_raw + L.loc);
   uint32_t* hz = reinterpret_cast<uint32_t*>(smem_raw + L.hz);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + L.bar);
   __shared__ uint32_t s_blk;
   __shared__ uint32_t s_tmp[NT / 32 + 1];
   const int tid = threadIdx.x;
-  const uint64_t pol = l2_policy_last();
+  constexpr uint32_t SKB = T + 8;  // per-buffer stride (elements)
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t phase[2] = {0u, 0u};
+
+  // issue the loads of tile [g0, g0+tn) into buffer `bf`: TMA for the body,
+  // plain loads (returned in registers) for the head/tail elements
+  auto issue = [&](int bf, uint64_t g0, uint32_t tn, K& hkv, V& hvv, int& hpos) {
+    uint32_t ko, khead, kbody, vo = 0, vhead = 0, vbody = 0;
+    const uint32_t kbytes = tile_body<K>(g0, tn, ko, khead, kbody);
+    uint32_t vbytes = 0;
+    if (VB) vbytes = tile_body<V>(g0, tn, vo, vhead, vbody);
+    if (tid == 0) {
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&bar[bf], kbytes + vbytes);
+      if (kbytes) tma_load_1d(skb + bf * SKB + ko + khead, kin + g0 + khead, kbytes, &bar[bf]);
+      if (vbytes) tma_load_1d(svb + bf * SKB + vo + vhead, vin + g0 + vhead, vbytes, &bar[bf]);
+    }
+    // head/tail: element positions not covered by the bulk copies
+    hpos = -1;
+    const uint32_t ktail = tn - khead - kbody;
+    const uint32_t nk = khead + ktail;
+    const uint32_t nv = VB ? vhead + (tn - vhead - vbody) : 0;
+    if ((uint32_t)tid < nk) {
+      const uint32_t e = (uint32_t)tid < khead ? (uint32_t)tid : khead + kbody + (tid - khead);
+      hkv = kin[g0 + e];
+      hpos = (int)e;
+    }
+    if (VB && (uint32_t)tid >= 64 && (uint32_t)tid < 64 + nv) {
+      const uint32_t t2 = tid - 64;
+      const uint32_t e = t2 < vhead ? t2 : vhead + vbody + (t2 - vhead);
+      hvv = vin[g0 + e];
+      hpos = (int)e;
+    }
+  };
+  auto commit_ht = [&](int bf, uint64_t g0, K hkv, V hvv, int hpos) {
+    if (hpos < 0) return;
+    if ((uint32_t)tid < 64) {
+      skb[bf * SKB + (uint32_t)(g0 % (16 / sizeof(K))) + hpos] = hkv;
+    } else if (VB) {
+      svb[bf * SKB + (uint32_t)(g0 % (16 / (VB ? VB : 4))) + hpos] = hvv;
+    }
+  };
 
   for (;;) {
     if (tid == 0) s_blk = atomicAdd(ctr, 1u);
@@ -200,30 +286,51 @@ __global__ void __launch_bounds__(NT, 2) k_scatter(const SegPlan* __restrict__ p
       for (uint32_t b = tid; b < nb; b += NT) {
         run[b] = rb + col[(uint64_t)b * P.nrows];
         tst[b] = 0;
+        loc[b] = 0;
       }
     }
-    __syncthreads();
     const Router<K> R = make_router<K>(P, hz, hk);
     SplitRouter<K> SR;
     SR.sk = hk; SR.si = si; SR.ns = P.nheavy;
     const int nbits = max(1, (int)ceil_log2_u64(nb));
-    const int npass = (nbits + 5) / 6;
+    const int npass = (nbits + 4) / 5;
     const int pbits = (nbits + npass - 1) / npass;
 
-    for (uint64_t tile = B.begin; tile < B.end; tile += T) {
-      const uint64_t rem_ = B.end - tile;
-      const uint32_t tn = rem_ < (uint64_t)T ? (uint32_t)rem_ : (uint32_t)T;
-      const uint32_t ko = stage_tile<K, NT>(sk, kin, tile, tn);
-      uint32_t vo = 0;
-      if (VB) vo = stage_tile<V, NT>(sv, vin, tile, tn);
-      __syncthreads();
+    const uint64_t ntile = (B.end - B.begin + T - 1) / T;
+    K hkv = 0;
+    V hvv = 0;
+    int hpos = -1;
+    {
+      const uint64_t g0 = B.begin;
+      const uint32_t tn = (uint32_t)min((uint64_t)T, B.end - g0);
+      issue(0, g0, tn, hkv, hvv, hpos);
+      commit_ht(0, g0, hkv, hvv, hpos);
+    }
+    __syncthreads();
+    for (uint64_t ti = 0; ti < ntile; ++ti) {
+      const int cb = (int)(ti & 1);
+      const uint64_t tile = B.begin + ti * T;
+      const uint32_t tn = (uint32_t)min((uint64_t)T, B.end - tile);
+      // prefetch the next tile of this block into the other buffer
+      const bool has_next = ti + 1 < ntile;
+      uint64_t ng0 = tile + T;
+      if (has_next) {
+        const uint32_t ntn = (uint32_t)min((uint64_t)T, B.end - ng0);
+        issue(cb ^ 1, ng0, ntn, hkv, hvv, hpos);
+      }
+      mbar_wait(&bar[cb], phase[cb]);
+      phase[cb] ^= 1u;
+      const uint32_t ko = (uint32_t)(tile % (16 / sizeof(K)));
+      const uint32_t vo = VB ? (uint32_t)(tile % (16 / (VB ? VB : 4))) : 0u;
+      const K* sk = skb + cb * SKB + ko;
+      const V* sv = svb + cb * SKB + vo;
       // route (blocked order) + tile histogram
       uint32_t w[IPT];
 #pragma unroll
       for (int i = 0; i < IPT; ++i) {
         const uint32_t e = tid * IPT + i;
         if (e < tn) {
-          const K key = sk[ko + e];
+          const K key = sk[e];
           const uint32_t b = SPLIT ? SR(key, global_base + tile + e) : R(key);
           atomicAdd(&tst[b], 1u);
           w[i] = (b << 16) | e;
@@ -248,21 +355,63 @@ __global__ void __launch_bounds__(NT, 2) k_scatter(const SegPlan* __restrict__ p
           for (int i = 0; i < IPT; ++i) w[i] = pk[tid * IPT + i];
         }
       }
-      // tile bucket starts (tst holds counts)
       block_exscan<NT>(tst, (int)nb, s_tmp);
       if (tid == 0) tst[nb] = tn;
       __syncthreads();
+      // W1: per bucket, flush limit F (whole sectors) and old leftovers
+      for (uint32_t b = tid; b < nb; b += NT) {
+        const uint32_t c = tst[b + 1] - tst[b];
+        const uint64_t r = run[b];
+        const uint32_t lc = loc[b];
+        const uint64_t end = r + c;
+        uint64_t F = end & ~AM;
+        if (lc == 0 && (r & AM) && end <= ((r + AM) & ~AM)) F = end;  // block's head sector
+        fl[b] = (int32_t)((int64_t)F - (int64_t)r);
+        const uint64_t lo0 = r - lc;
+        for (uint32_t s = 0; s < lc; ++s) {
+          const uint64_t d = lo0 + s;
+          if (d < F) {
+            kout[d] = lk[b * A + s];
+            if (VB) vout[d] = lv[b * A + s];
+          } else {
+            lk[b * A + (d - F)] = lk[b * A + s];
+            if (VB) lv[b * A + (d - F)] = lv[b * A + s];
+          }
+        }
+        loc[b] = (uint8_t)(end - F);
+        run[b] = end;
+      }
+      __syncthreads();
+      // W2: tile records -> global (flushable) or leftover buffer
       for (uint32_t p = tid; p < tn; p += NT) {
         const uint32_t wd = pk[p];
         const uint32_t b = wd >> 16, e = wd & 0xffffu;
-        const uint64_t d = run[b] + (p - tst[b]);
-        st_keep(kout + d, sk[ko + e], pol);
-        if (VB) st_keep(vout + d, sv[vo + e], pol);
+        const int32_t dr = (int32_t)(p - tst[b]);
+        const int32_t f = fl[b];
+        if (dr < f) {
+          const uint64_t d = run[b] - (tst[b + 1] - tst[b]) + (uint32_t)dr;
+          kout[d] = sk[e];
+          if (VB) vout[d] = sv[e];
+        } else {
+          const uint32_t s = (uint32_t)(dr - f);
+          lk[b * A + s] = sk[e];
+          if (VB) lv[b * A + s] = sv[e];
+        }
       }
-      __syncthreads();
-      for (uint32_t b = tid; b < nb; b += NT) run[b] += tst[b + 1] - tst[b];
+      if (has_next) commit_ht(cb ^ 1, ng0, hkv, hvv, hpos);
       __syncthreads();
       for (uint32_t b = tid; b < nb; b += NT) tst[b] = 0;
+      // (the next tile's route phase follows a barrier inside mbar/route)
+      __syncthreads();
+    }
+    // block end: flush the remaining partial sectors
+    for (uint32_t b = tid; b < nb; b += NT) {
+      const uint32_t lc = loc[b];
+      const uint64_t lo0 = run[b] - lc;
+      for (uint32_t s = 0; s < lc; ++s) {
+        kout[lo0 + s] = lk[b * A + s];
+        if (VB) vout[lo0 + s] = lv[b * A + s];
+      }
     }
     __syncthreads();
   }

@@ -1,0 +1,206 @@
+"""GPU parity: the CUDA path (through the public API / the C ABI) against the
+reference's golden outputs and the CPU oracle.  Bit-exact for every key and
+payload (integer work: no tolerance)."""
+import json
+import pathlib
+
+import numpy as np
+import pytest
+
+import cases
+from oracle import oracle as ora
+
+pytestmark = pytest.mark.gpu
+
+G = pathlib.Path(__file__).resolve().parent / "golden"
+GOLD = json.loads((G / "sort_golden.json").read_text())
+
+
+def _sorters():
+    from paper_2401_00710_b200 import dt_sort, plain_msd_sort
+
+    return {"dt": dt_sort, "plain": plain_msd_sort}
+
+
+@pytest.mark.parametrize("case", GOLD["cases"], ids=[c["name"] for c in GOLD["cases"]])
+def test_gpu_matches_reference_golden(case):
+    from paper_2401_00710_b200 import RecordArray, SortConfig
+
+    keys, pays = cases.make_input(case)
+    for mode, fn in _sorters().items():
+        rec = RecordArray(keys.copy(), None if pays is None else pays.copy())
+        ret = fn(rec, SortConfig(**case["cfg"]))
+        assert ret is None
+        assert cases.sha(rec.keys, rec.payloads) == case[f"{mode}_sha"], mode
+
+
+def test_gpu_known_answer_c1_and_c2_shape():
+    from paper_2401_00710_b200 import RecordArray, dt_sort
+
+    c1 = np.random.default_rng(0).integers(0, 2**32, size=10**6, dtype=np.uint32)
+    rec = RecordArray(c1.copy())
+    dt_sort(rec)
+    assert cases.sha(rec.keys) == GOLD["known"]["c1"]["output_sha"]
+    c2k = np.random.default_rng(0).integers(0, 10**9, size=10**6, dtype=np.uint32)
+    rec = RecordArray(c2k.copy(), np.arange(10**6, dtype=np.uint32))
+    dt_sort(rec)
+    kn = GOLD["known"]["c2_1e6"]
+    assert cases.sha(rec.keys) == kn["keys_sha"]
+    assert cases.sha(rec.payloads) == kn["vals_u32_sha"]
+
+
+WIDTHS = [(4, 0), (4, 4), (4, 8), (8, 0), (8, 4), (8, 8)]
+
+
+@pytest.mark.parametrize("kb,vb", WIDTHS)
+@pytest.mark.parametrize("dist", ["full", "few", "zipf", "planted", "exp", "bexp", "small16",
+                                  "sorted", "reversed", "const"])
+@pytest.mark.parametrize("n", [1, 3, 4353, 100_003, 1_000_000])
+def test_gpu_matches_oracle_widths(kb, vb, dist, n):
+    from paper_2401_00710_b200 import RecordArray, dt_sort, plain_msd_sort
+
+    rng = np.random.default_rng(n * 7 + kb + vb)
+    keys = cases._dist(dist, n, kb * 8, rng)
+    vdt = {0: None, 4: np.uint32, 8: np.uint64}[vb]
+    vals = None if vdt is None else rng.integers(0, 2**31, size=n).astype(vdt)
+    want_k, want_v = ora.reference_sort(keys, vals)
+    for fn in (dt_sort, plain_msd_sort):
+        rec = RecordArray(keys.copy(), None if vals is None else vals.copy())
+        fn(rec)
+        assert np.array_equal(rec.keys, want_k), fn.__name__
+        if vals is not None:
+            assert np.array_equal(rec.payloads, want_v), fn.__name__
+
+
+@pytest.mark.parametrize("cfg", [dict(gamma_lo=4, gamma_hi=4, base_case_threshold=16),
+                                 dict(gamma_lo=1, gamma_hi=2, base_case_threshold=4),
+                                 dict(theory_mode=True, base_case_exponent=2, gamma_lo=4, gamma_hi=4),
+                                 dict(gamma_lo=12, gamma_hi=12)])
+@pytest.mark.parametrize("dist", ["full", "few", "planted", "zipf"])
+def test_gpu_deep_recursion_configs(cfg, dist):
+    from paper_2401_00710_b200 import RecordArray, SortConfig, dt_sort
+
+    rng = np.random.default_rng(5)
+    for width in (32, 64):
+        keys = cases._dist(dist, 60_000, width, rng)
+        pays = np.arange(keys.shape[0], dtype=np.uint64)
+        want_k, want_v = ora.dt_sort(keys, pays)
+        rec = RecordArray(keys.copy(), pays.copy())
+        dt_sort(rec, SortConfig(**cfg))
+        assert np.array_equal(rec.keys, want_k) and np.array_equal(rec.payloads, want_v)
+
+
+def test_gpu_torch_inputs_in_place():
+    import torch
+
+    from paper_2401_00710_b200 import RecordArray, SortConfig, dt_sort
+
+    rng = np.random.default_rng(9)
+    keys = rng.integers(0, 2**32, size=300_000, dtype=np.uint64).astype(np.uint32)
+    keys[::3] = 12345
+    vals = np.arange(keys.shape[0], dtype=np.uint32)
+    want_k, want_v = ora.dt_sort(keys, vals)
+    # CUDA tensors: sorted in place, same objects
+    dk = torch.from_numpy(keys.copy()).cuda()
+    dv = torch.from_numpy(vals.copy()).cuda()
+    p0 = dk.data_ptr()
+    rep = dt_sort(RecordArray(dk, dv), SortConfig(instrument=True))
+    assert dk.data_ptr() == p0
+    assert np.array_equal(dk.cpu().numpy(), want_k) and np.array_equal(dv.cpu().numpy(), want_v)
+    assert rep.level_mass[0] == keys.shape[0] and rep.gpu_launches > 0
+    # CPU tensors (pinned and pageable)
+    for pin in (True, False):
+        hk = torch.from_numpy(keys.copy())
+        hv = torch.from_numpy(vals.copy())
+        if pin:
+            hk, hv = hk.pin_memory(), hv.pin_memory()
+        dt_sort(RecordArray(hk, hv))
+        assert np.array_equal(hk.numpy(), want_k) and np.array_equal(hv.numpy(), want_v)
+    # non-contiguous CUDA view
+    big = torch.from_numpy(np.stack([keys, keys]).T.copy()).cuda()
+    view = big[:, 0]
+    assert not view.is_contiguous()
+    dt_sort(RecordArray(view))
+    assert np.array_equal(view.cpu().numpy(), want_k)
+    assert np.array_equal(big[:, 1].cpu().numpy(), keys)  # neighbour column untouched
+
+
+def test_gpu_numpy_in_place_identity_and_report():
+    from paper_2401_00710_b200 import RecordArray, SortConfig, dt_sort
+
+    rng = np.random.default_rng(2)
+    rec = RecordArray(rng.integers(0, 99, size=5000).astype(np.uint32),
+                      np.arange(5000, dtype=np.uint64))
+    k, p = rec.keys, rec.payloads
+    assert dt_sort(rec) is None
+    assert rec.keys is k and rec.payloads is p
+    rep = dt_sort(rec, SortConfig(instrument=True))
+    assert rep is not None and rep.level_mass[0] == 5000
+
+
+def test_gpu_stability_direct():
+    from paper_2401_00710_b200 import RecordArray, dt_sort
+
+    keys = np.tile(np.array([5, 1, 5, 1, 9], np.uint32), 40_000)
+    rec = RecordArray(keys.copy(), np.arange(keys.shape[0], dtype=np.uint64))
+    dt_sort(rec)
+    for v in (1, 5, 9):
+        group = rec.payloads[rec.keys == v]
+        assert np.all(np.diff(group.astype(np.int64)) > 0)
+
+
+def test_gpu_heavy_keys_and_overflow_counters():
+    from paper_2401_00710_b200 import RecordArray, SortConfig, dt_sort
+
+    rng = np.random.default_rng(7)
+    n = 2_000_000
+    keys = rng.integers(0, 1 << 20, size=n, dtype=np.uint32)
+    keys[: n // 3] = 0x1234
+    keys[rng.integers(0, n, size=3)] = np.array([1 << 30, (1 << 32) - 1, 1 << 28], np.uint32)
+    rng.shuffle(keys)
+    pays = np.arange(n, dtype=np.uint32)
+    want_k, want_v = ora.dt_sort(keys, pays)
+    rec = RecordArray(keys.copy(), pays.copy())
+    rep = dt_sort(rec, SortConfig(instrument=True))
+    assert np.array_equal(rec.keys, want_k) and np.array_equal(rec.payloads, want_v)
+    assert rep.heavy_records_removed[0] >= n // 3  # the planted key got its own bucket
+    assert rep.records_distributed >= n
+
+
+def test_gpu_thread_count_invariance():
+    from paper_2401_00710_b200 import RecordArray, SortConfig, dt_sort, set_num_workers
+
+    rng = np.random.default_rng(3)
+    keys = rng.integers(0, 1 << 32, size=200_000, dtype=np.uint64).astype(np.uint32)
+    keys[:50_000] = 0xDEADBEEF
+    rng.shuffle(keys)
+    base = None
+    for w in (1, 2, 8):
+        set_num_workers(w)
+        rec = RecordArray(keys.copy(), np.arange(keys.shape[0], dtype=np.uint64))
+        rep = dt_sort(rec, SortConfig(instrument=True))
+        got = (rec.tobytes(), rep.structural())
+        base = base or got
+        assert got == base
+    set_num_workers(None)
+
+
+def test_gpu_large_c2_certificate():
+    """C2 shape at 10^8 on the device: the O(n) stable-sort certificate."""
+    import torch
+
+    from paper_2401_00710_b200 import SortConfig
+    from paper_2401_00710_b200.dtsort import sort_device
+
+    n = 10**8
+    g = torch.Generator(device="cuda")
+    g.manual_seed(0)
+    k0 = torch.randint(0, 10**9, (n,), generator=g, device="cuda", dtype=torch.int32)
+    k = k0.clone()
+    v = torch.arange(n, device="cuda", dtype=torch.int32)
+    sort_device(k, v, SortConfig(), 0)
+    assert bool((k[1:] >= k[:-1]).all())
+    eq = k[1:] == k[:-1]
+    assert bool((v[1:][eq] > v[:-1][eq]).all())
+    assert bool((k0[v.long()] == k).all())
+    assert int(torch.bincount(v.long(), minlength=n).max()) == 1
