@@ -16,7 +16,8 @@
 #include <vector>
 
 #include "../../include/dts.h"
-#include "dts_sort_kernels.cuh"
+#include "dts_local.cuh"
+#include "dts_scatter.cuh"
 
 using namespace dts;
 
@@ -46,11 +47,7 @@ int fail(int code, const std::string& msg) {
 // Tunables (B200-sized)
 // ---------------------------------------------------------------------------
 constexpr int HIST_NT = 512;
-constexpr int LOCAL_NT = 256;
-constexpr int LOCAL_IPT = 17;
-constexpr int LOCAL_RB = 5;                    // radix bits per local-sort pass
 constexpr int SAMPLE_NT = 1024;
-constexpr uint32_t GMAX_HW = 10;               // widest digit the scatter is sized for
 constexpr uint64_t BLOCK_RECORDS = 1u << 18;   // records per count-matrix row
 constexpr uint32_t COPY_CHUNK = 1u << 16;
 constexpr uint64_t SPAN_BATCH = 1u << 18;      // spans per k_local_sort launch
@@ -64,7 +61,6 @@ int env_int(const char* name, int dflt) {
 }
 
 // Local-sort capacity per record width (SMEM ~ CAP*(kb+vb+2) bytes).
-inline int local_cap(int, int) { return LOCAL_NT * LOCAL_IPT; }
 
 // ---------------------------------------------------------------------------
 // Pinned host staging (grown on demand at sync points)
@@ -244,6 +240,7 @@ struct Sorter {
   int cap;        // local-sort capacity (records)
   uint64_t thr;   // base-case threshold (records <= thr -> k_local_sort)
   uint32_t gcap, glo;
+  uint32_t gcap_hw;  // log2 of the scatter's bucket capacity
   uint32_t stride;  // ceil_log2(n) (sampler.py:121-127)
   uint32_t gs_max, smax;
 
@@ -268,7 +265,7 @@ struct Sorter {
   // segment holds at least SAMPLE_FACTOR x the sample).  Adjusts g (<= 9)
   // and returns the subsample exponent gs (|S| = 2^gs * stride).
   bool sampled_plan(uint64_t len, uint32_t remaining, uint32_t& g, uint32_t& gs) const {
-    const uint32_t g9 = std::min<uint32_t>(g, 9);
+    const uint32_t g9 = std::min<uint32_t>(g, gcap_hw > 1 ? gcap_hw - 1 : 1);
     gs = std::min<uint32_t>(g9 > 1 ? g9 - 1 : 1, gs_max);
     uint64_t S = std::min<uint64_t>(len, (uint64_t(1) << gs) * stride);
     S = std::min<uint64_t>(S, smax);
@@ -323,10 +320,11 @@ struct Sorter {
       Timer::Ev ev;
       tm.begin(DTS_K_LOCAL, ev);
       {
-        auto fn = k_local_sort<K, VB, LOCAL_NT, LOCAL_IPT, LOCAL_RB>;
-        const size_t sm = local_layout(LOCAL_NT * LOCAL_IPT, LOCAL_NT, sizeof(K), VB, LOCAL_RB).total;
+        using LT = LocalTile<K, VB>;
+        auto fn = k_local_sort<K, VB>;
+        const size_t sm = local_layout(LT::CAP, LT::NT, sizeof(K), VB, LT::FAST_BITS).total;
         DTS_TRY(set_smem(fn, sm));
-        fn<<<(unsigned)cnt, LOCAL_NT, sm, st>>>(dsp, Ak, Av, Tk, Tv);
+        fn<<<(unsigned)cnt, LT::NT, sm, st>>>(dsp, Ak, Av, Tk, Tv);
       }
       tm.end(ev, recs);
       DTS_TRY(check_launch("k_local_sort"));
@@ -629,11 +627,13 @@ int sort_impl(void* keys, void* vals, uint64_t n, void* ws, size_t wsb, const dt
   S.cfg = *cfg;
   S.rep = rep;
   S.st = st;
-  S.cap = local_cap(sizeof(K), VB);
+  S.cap = LocalTile<K, VB>::CAP;
   // theta: SortConfig.effective_theta (core.py:148-151), capped by SMEM.
   uint64_t theta = cfg->base_case_threshold;
+  const uint32_t gcap_hw = ceil_log2_u64(ScatterTile<K, VB>::NBC);
   uint32_t gcap = std::min<uint32_t>((uint32_t)std::max(1, cfg->gamma_hi),
-                                     (uint32_t)env_int("DTS_GMAX", GMAX_HW));
+                                     (uint32_t)env_int("DTS_GMAX", (int)gcap_hw));
+  gcap = std::min(gcap, gcap_hw);
   gcap = std::max<uint32_t>(1, std::min<uint32_t>(gcap, 12));
   if (cfg->theory_mode) {
     const uint64_t e = (uint64_t)std::max(1, cfg->base_case_exponent) * gcap;
@@ -645,6 +645,7 @@ int sort_impl(void* keys, void* vals, uint64_t n, void* ws, size_t wsb, const dt
   if (thr < 1) thr = 1;
   S.thr = thr;
   S.gcap = gcap;
+  S.gcap_hw = gcap_hw;
   S.glo = (uint32_t)std::max(1, cfg->gamma_lo);
   S.stride = n <= 2 ? 1 : ceil_log2_u64(n);
   S.gs_max = sizeof(K) == 4 ? 10 : 9;

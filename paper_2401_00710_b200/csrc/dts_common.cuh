@@ -334,6 +334,67 @@ __device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], const int
   for (int i = 0; i < IPT; ++i) rank[i] += cnt[dig[i] * NT + t];
 }
 
+// Packed variant (CUB-style): u32 counter words laid out [lane][thread],
+// lane = d mod H (H = D/2), each word packing the u16 counts of digits
+// `lane` (low half) and `lane + H` (high half).  The digit-major scan then
+// runs on packed words (both halves at once), and high-half digits add the
+// low-half grand total.  `addr` caches each item's counter word index.
+template <int NT, int IPT>
+__device__ __forceinline__ void block_rank_packed(const uint32_t (&dig)[IPT], const int hbits,
+                                                  uint32_t (&rank)[IPT], uint32_t* cnt,
+                                                  uint32_t* tmp) {
+  const int t = threadIdx.x;
+  const int H = 1 << hbits;  // D = 2H digit values
+  uint32_t* col = cnt + t;
+  for (int l = 0; l < H; ++l) col[l * NT] = 0u;
+  uint32_t widx[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const uint32_t d = dig[i];
+    const uint32_t sh = (d >> hbits) << 4;
+    widx[i] = (d & (uint32_t)(H - 1)) * NT;
+    const uint32_t w = col[widx[i]];
+    rank[i] = (w >> sh) & 0xffffu;
+    col[widx[i]] = w + (1u << sh);
+  }
+  __syncthreads();
+  // raking scan: thread t owns packed words [t*H, t*H + H) of the [lane][thread] array
+  uint32_t* mine = cnt + t * H;
+  uint32_t sum = 0;
+  if (H >= 4) {
+    for (int k = 0; k < H; k += 4) {
+      const uint4 q = *reinterpret_cast<const uint4*>(mine + k);
+      sum += q.x + q.y + q.z + q.w;
+    }
+  } else {
+    for (int k = 0; k < H; ++k) sum += mine[k];
+  }
+  uint32_t total;
+  uint32_t run = block_exscan_val<NT>(sum, tmp, &total);
+  if (H >= 4) {
+    for (int k = 0; k < H; k += 4) {
+      uint4 q = *reinterpret_cast<const uint4*>(mine + k);
+      const uint32_t a = run, b = a + q.x, c = b + q.y, e = c + q.z;
+      run = e + q.w;
+      *reinterpret_cast<uint4*>(mine + k) = make_uint4(a, b, c, e);
+    }
+  } else {
+    for (int k = 0; k < H; ++k) {
+      const uint32_t v = mine[k];
+      mine[k] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  const uint32_t lo_total = total & 0xffffu;
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const uint32_t hi = dig[i] >> hbits;
+    const uint32_t w = col[widx[i]];
+    rank[i] += ((w >> (hi << 4)) & 0xffffu) + (hi ? lo_total : 0u);
+  }
+}
+
 // Block-wide exclusive scan of a[0..n) in shared memory (in place); returns
 // the total.  All threads of the block must call it.  `tmp` holds NT/32
 // entries.
