@@ -163,7 +163,8 @@ def test_gpu_heavy_keys_and_overflow_counters():
     rec = RecordArray(keys.copy(), pays.copy())
     rep = dt_sort(rec, SortConfig(instrument=True))
     assert np.array_equal(rec.keys, want_k) and np.array_equal(rec.payloads, want_v)
-    assert rep.heavy_records_removed[0] >= n // 3  # the planted key got its own bucket
+    # the planted key got its own bucket (3 outliers may overwrite planted slots)
+    assert rep.heavy_records_removed[0] >= n // 3 - 3
     assert rep.records_distributed >= n
 
 
