@@ -322,7 +322,7 @@ struct Sorter {
       {
         using LT = LocalTile<K, VB>;
         auto fn = k_local_sort<K, VB>;
-        const size_t sm = local_layout(LT::CAP, LT::NT, sizeof(K), VB, LT::FAST_BITS).total;
+        const size_t sm = local_layout(LT::CAP, LT::NT, sizeof(K), VB, LT::RB).total;
         DTS_TRY(set_smem(fn, sm));
         fn<<<(unsigned)cnt, LT::NT, sm, st>>>(dsp, Ak, Av, Tk, Tv);
       }

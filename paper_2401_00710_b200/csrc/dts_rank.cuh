@@ -15,6 +15,12 @@
 
 namespace dts {
 
+// Test hook: 1 forces the general in-step re-sort paths on every tile (the
+// fast path relies on a verified-but-unpromised atomic order).
+#ifndef DTS_FORCE_FIXUP
+#define DTS_FORCE_FIXUP 0
+#endif
+
 constexpr int FIXMAX = 64;  // small-bucket insertion-sort limit
 constexpr int NLARGE = 8;   // large buckets per tile with exact packed-prefix slots
 

@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 1)
   uint8_t* loc = reinterpret_cast<uint8_t*>(smem_raw + L.loc);
   uint32_t* hz = reinterpret_cast<uint32_t*>(smem_raw + L.hz);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + L.bar);
-  __shared__ uint32_t s_blk;
+  __shared__ uint32_t s_blk, s_fix;
   __shared__ uint32_t s_tmp[NW + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr uint32_t SKB = T + 8;  // per-buffer stride (elements)
@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 1)
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_mbar_init();
+    s_fix = 0u;
   }
   for (uint32_t i = tid; i < NW * HW; i += NT) wh[i] = 0u;
   __syncthreads();
@@ -249,31 +250,22 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 1)
         }
       }
       __syncthreads();
-      // ---- order lanes of one warp step that hit the same bucket: a group
-      // is (bucket, warp step) = (b, e >> 5); its records are contiguous ----
+      // ---- verify the in-step order.  Lanes of one warp step that hit the
+      // same bucket form a group (b, e >> 5) of contiguous records; the
+      // SMEM atomics gave them increasing ranks in lane order on every B200
+      // probed (tools/atomic_order.cu: 0 of 5e9 colliding pairs out of
+      // order), which the PTX model does not promise — so check each
+      // adjacent pair and re-sort groups only if one is out of order.
+      // The check runs in the same phase as W1 (no extra barrier). ----
       for (uint32_t i = tid; i < NW * HW; i += NT) wh[i] = 0u;
-      for (uint32_t p0 = 0; p0 < tn; p0 += NT) {
-        const uint32_t p = p0 + tid;
-        const uint32_t x = p < tn ? pk[p] : 0xFFFFFFFFu;
-        uint32_t prev = __shfl_up_sync(FULL, x, 1);
-        if (lane == 0) prev = p > 0 ? pk[p - 1] : 0xFFFFFFFFu;
-        uint32_t next = __shfl_down_sync(FULL, x, 1);
-        if (lane == 31) next = p + 1 < tn ? pk[p + 1] : 0xFFFFFFFFu;
-        const uint32_t g = (x >> 16 << 16) | ((x & 0xffffu) >> 5);
-        const uint32_t gp = (prev >> 16 << 16) | ((prev & 0xffffu) >> 5);
-        const uint32_t gn = (next >> 16 << 16) | ((next & 0xffffu) >> 5);
-        const bool leader = p < tn && (p == 0 || gp != g);
-        if (leader && p + 1 < tn && gn == g) {
-          uint32_t c = 2;
-          while (p + c < tn) {
-            const uint32_t y = pk[p + c];
-            if (((y >> 16 << 16) | ((y & 0xffffu) >> 5)) != g) break;
-            ++c;
-          }
-          small_isort(pk + p, c);
+      {
+        bool bad = false;
+        for (uint32_t p = tid; p + 1 < tn; p += NT) {
+          const uint32_t x = pk[p], y = pk[p + 1];
+          bad |= ((x ^ y) < 32u) && (y < x);  // same bucket & step, descending
         }
+        if (__any_sync(FULL, bad) && lane == 0) s_fix = 1u;
       }
-      __syncthreads();
       // ---- W1: per bucket, flush limit F (whole sectors), old leftovers ----
       for (uint32_t b = tid; b < nb; b += NT) {
         const uint32_t ts = tst[b];
@@ -286,33 +278,54 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 1)
         dbase[b] = r - ts;
         fl[b] = (int32_t)ts + (int32_t)((int64_t)F - (int64_t)r);
         const uint64_t lo0 = r - lc;
-        for (uint32_t s = 0; s < lc; ++s) {
-          const uint64_t d = lo0 + s;
+        for (uint32_t s2 = 0; s2 < lc; ++s2) {
+          const uint64_t d = lo0 + s2;
           if (d < F) {
-            kout[d] = lk[b * A + s];
-            if (VB) vout[d] = lv[b * A + s];
+            kout[d] = lk[b * A + s2];
+            if (VB) vout[d] = lv[b * A + s2];
           } else {
-            lk[b * A + (d - F)] = lk[b * A + s];
-            if (VB) lv[b * A + (d - F)] = lv[b * A + s];
+            lk[b * A + (d - F)] = lk[b * A + s2];
+            if (VB) lv[b * A + (d - F)] = lv[b * A + s2];
           }
         }
         loc[b] = (uint8_t)(end - F);
         run[b] = end;
       }
       __syncthreads();
+      if (s_fix || DTS_FORCE_FIXUP) {
+        // general path: sort every group (b, e >> 5) of >= 2 records by e
+        for (uint32_t p = tid; p < tn; p += NT) {
+          const uint32_t x = pk[p];
+          const bool leader = p == 0 || ((pk[p - 1] ^ x) >= 32u);
+          if (leader && p + 1 < tn && ((pk[p + 1] ^ x) < 32u)) {
+            uint32_t c = 2;
+            while (p + c < tn && ((pk[p + c] ^ x) < 32u)) ++c;
+            small_isort(pk + p, c);
+          }
+        }
+        __syncthreads();
+        if (tid == 0) s_fix = 0u;
+      }
       // ---- W2: tile records -> global (flushable) or leftover buffer ----
-      for (uint32_t p = tid; p < tn; p += NT) {
-        const uint32_t wd = pk[p];
-        const uint32_t b = wd >> 16, e = wd & 0xffffu;
-        const int32_t lim = fl[b];
-        if ((int32_t)p < lim) {
-          const uint64_t d = dbase[b] + p;
-          kout[d] = sk[e];
-          if (VB) vout[d] = sv[e];
-        } else {
-          const uint32_t s = (uint32_t)((int32_t)p - lim);
-          lk[b * A + s] = sk[e];
-          if (VB) lv[b * A + s] = sv[e];
+#pragma unroll
+      for (int it = 0; it < IPT; ++it) {
+        const uint32_t p = it * NT + tid;
+        if (p < tn) {
+          const uint32_t wd = pk[p];
+          const uint32_t b = wd >> 16, e = wd & 0xffffu;
+          const int32_t lim = fl[b];
+          const K kv = sk[e];
+          V vv = 0;
+          if (VB) vv = sv[e];
+          if ((int32_t)p < lim) {
+            const uint64_t d = dbase[b] + p;
+            kout[d] = kv;
+            if (VB) vout[d] = vv;
+          } else {
+            const uint32_t s = (uint32_t)((int32_t)p - lim);
+            lk[b * A + s] = kv;
+            if (VB) lv[b * A + s] = vv;
+          }
         }
       }
       if (has_next) commit_ht(cb ^ 1, ng0, hkv, hvv, hpos);
