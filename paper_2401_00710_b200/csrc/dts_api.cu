@@ -196,7 +196,13 @@ struct Bump {
   }
 };
 
-size_t meta_bytes(uint64_t n) { return (size_t(48) << 20) + (size_t)(n / 4); }
+// Level metadata bound: count matrix / scan / bounds (~n/4 B) plus the
+// scatter's look-back status (one u32 per tile per bucket column; tiles hold
+// >= 2560 records, columns <= 1024) — about 1.9 B per record at most.
+size_t meta_bytes(uint64_t n) {
+  const uint64_t tiles = n / 2560 + n / BLOCK_RECORDS + 2;
+  return (size_t(64) << 20) + (size_t)(n / 4) + (size_t)(tiles * 1024 * 4);
+}
 
 struct HostSeg {
   uint64_t offset, len;
@@ -416,6 +422,19 @@ struct Sorter {
     }
     nbc = (nbc + 1) & ~1u;
     Caps caps{nbc, hzc, hkc, 0};
+    // scatter tiles in input order (each hist block split into T-record tiles)
+    constexpr uint32_t ST_T = ScatterTile<K, VB>::T;
+    std::vector<uint32_t> blk_tile0(blks.size());
+    uint64_t ntile = 0;
+    for (size_t bi = 0; bi < blks.size(); ++bi) {
+      blk_tile0[bi] = (uint32_t)ntile;
+      ntile += (blks[bi].end - blks[bi].begin + ST_T - 1) / ST_T;
+    }
+    std::vector<uint32_t> tile_blk(ntile);
+    for (size_t bi = 0; bi < blks.size(); ++bi) {
+      const uint32_t e = bi + 1 < blks.size() ? blk_tile0[bi + 1] : (uint32_t)ntile;
+      for (uint32_t t = blk_tile0[bi]; t < e; ++t) tile_blk[t] = (uint32_t)bi;
+    }
 
     // ---- device meta ----
     const size_t save = meta.off;
@@ -431,18 +450,27 @@ struct Sorter {
     K* dheavy = (K*)meta.take(std::max<uint64_t>(1, heavy_total) * sizeof(K));
     uint32_t* dhz = (uint32_t*)meta.take(std::max<uint64_t>(1, hz_total) * 4);
     uint32_t* dctr = (uint32_t*)meta.take(16);
+    uint32_t* dtile_blk = (uint32_t*)meta.take(std::max<uint64_t>(1, ntile) * 4);
+    uint32_t* dblk_tile0 = (uint32_t*)meta.take(std::max<size_t>(1, blks.size()) * 4);
+    uint32_t* dstatus = (uint32_t*)meta.take(std::max<uint64_t>(1, ntile) * nbc * 4);
     if (!dplans || !dblks || !dsampled || !dcnt || !dscan || !dpart || !dbs || !dkinds ||
-        !dheavy || !dhz || !dctr)
+        !dheavy || !dhz || !dctr || !dtile_blk || !dblk_tile0 || !dstatus)
       return fail(DTS_ENOMEM, "workspace too small for level metadata");
 
     // ---- H2D ----
     const size_t pb = ns * sizeof(SegPlan), bb = blks.size() * sizeof(Blk),
                  sb = sampled.size() * 4;
-    DTS_TRY(g_pin_plan.ensure(align256(pb) + align256(bb) + sb + 256));
+    const size_t tb = ntile * 4, b0b = blks.size() * 4;
+    DTS_TRY(g_pin_plan.ensure(align256(pb) + align256(bb) + align256(sb) + align256(tb) + b0b + 512));
     char* hp = (char*)g_pin_plan.p;
     std::memcpy(hp, plans.data(), pb);
     std::memcpy(hp + align256(pb), blks.data(), bb);
     if (sb) std::memcpy(hp + align256(pb) + align256(bb), sampled.data(), sb);
+    char* htl = hp + align256(pb) + align256(bb) + align256(sb);
+    std::memcpy(htl, tile_blk.data(), tb);
+    std::memcpy(htl + align256(tb), blk_tile0.data(), b0b);
+    CUDA_TRY(cudaMemcpyAsync(dtile_blk, htl, tb, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dblk_tile0, htl + align256(tb), b0b, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(dplans, hp, pb, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(dblks, hp + align256(pb), bb, cudaMemcpyHostToDevice, st));
     if (sb)
@@ -494,15 +522,17 @@ struct Sorter {
     // ---- scatter ----
     {
       CUDA_TRY(cudaMemsetAsync(dctr + 1, 0, 4, st));
+      CUDA_TRY(cudaMemsetAsync(dstatus, 0, ntile * nbc * 4, st));
       Timer::Ev ev;
       tm.begin(DTS_K_SCATTER, ev);
       using TL = ScatterTile<K, VB>;
       auto fn = k_scatter<K, VB, false>;
-      const size_t sm = scatter_layout(TL::T, TL::NT, TL::A, sizeof(K), VB, caps, false).total;
+      const size_t sm = scatter_layout(TL::T, TL::NT, sizeof(K), VB, caps, false).total;
       DTS_TRY(set_smem(fn, sm));
-      const int grid = persistent_grid(fn, TL::NT, sm, (uint32_t)blks.size());
-      fn<<<grid, TL::NT, sm, st>>>(dplans, dblks, (uint32_t)blks.size(), dctr + 1, ink, inv,
-                                    outk, outv, dscan, dheavy, dhz, nullptr, 0, caps);
+      const int grid = persistent_grid(fn, TL::NT, sm, (uint32_t)ntile);
+      fn<<<grid, TL::NT, sm, st>>>(dplans, dblks, dtile_blk, dblk_tile0, (uint32_t)ntile,
+                                    dctr + 1, ink, inv, outk, outv, dscan, dstatus, dheavy, dhz,
+                                    nullptr, 0, caps);
       tm.end(ev, wave_recs);
       DTS_TRY(check_launch("k_scatter"));
     }
@@ -568,7 +598,9 @@ struct Sorter {
     const uint64_t rows = std::max<uint64_t>(1, (s.len + BLOCK_RECORDS - 1) / BLOCK_RECORDS);
     const uint32_t g = choose_gamma(s.len, W - s.consumed);
     const uint64_t nbmax = (1u << g) + (1u << std::min(g, gs_max)) + 1u;
-    return 88 + rows * 24 + nbmax * rows * 12 + (nbmax + 1) * 9 + (1u << g) * 12 + 4096;
+    const uint64_t tiles = s.len / 2560 + rows + 1;
+    return 88 + rows * 28 + nbmax * rows * 12 + (nbmax + 1) * 9 + (1u << g) * 12 + 4096 +
+           tiles * (4 + ((nbmax + 1) & ~1ull) * 4);
   }
 
   int run() {
@@ -582,7 +614,7 @@ struct Sorter {
     int level = 0;
     bool in_T = false;
     // the span/copy descriptor area must stay available after a wave
-    const size_t budget = meta.cap / 2;
+    const size_t budget = meta.cap > (size_t(24) << 20) ? meta.cap - (size_t(16) << 20) : meta.cap / 2;
     while (!segs.empty()) {
       std::vector<HostSeg> next;
       size_t s0 = 0;
@@ -703,14 +735,37 @@ int partition_impl(const void* keys, const void* vals, uint64_t n, uint64_t gbas
   K* dsk = (K*)meta.take(std::max(1, nsplit) * sizeof(K));
   uint64_t* dsi = (uint64_t*)meta.take(std::max(1, nsplit) * 8);
   uint32_t* dctr = (uint32_t*)meta.take(16);
-  if (!dplan || !dblks || !dcnt || !dscan || !dpart || !dbs || !dkinds || !dsk || !dsi || !dctr)
+  constexpr uint32_t ST_T = ScatterTile<K, VB>::T;
+  std::vector<uint32_t> blk_tile0(blks.size());
+  uint64_t ntile = 0;
+  for (size_t bi = 0; bi < blks.size(); ++bi) {
+    blk_tile0[bi] = (uint32_t)ntile;
+    ntile += (blks[bi].end - blks[bi].begin + ST_T - 1) / ST_T;
+  }
+  std::vector<uint32_t> tile_blk(ntile);
+  for (size_t bi = 0; bi < blks.size(); ++bi) {
+    const uint32_t e = bi + 1 < blks.size() ? blk_tile0[bi + 1] : (uint32_t)ntile;
+    for (uint32_t t = blk_tile0[bi]; t < e; ++t) tile_blk[t] = (uint32_t)bi;
+  }
+  const uint32_t nbc = (G + 1) & ~1u;
+  uint32_t* dtile_blk = (uint32_t*)meta.take(std::max<uint64_t>(1, ntile) * 4);
+  uint32_t* dblk_tile0 = (uint32_t*)meta.take(std::max<size_t>(1, blks.size()) * 4);
+  uint32_t* dstatus = (uint32_t*)meta.take(std::max<uint64_t>(1, ntile) * nbc * 4);
+  if (!dplan || !dblks || !dcnt || !dscan || !dpart || !dbs || !dkinds || !dsk || !dsi || !dctr ||
+      !dtile_blk || !dblk_tile0 || !dstatus)
     return fail(DTS_ENOMEM, "workspace too small for partition metadata");
   const size_t bb = blks.size() * sizeof(Blk);
-  DTS_TRY(g_pin_plan.ensure(512 + align256(bb) + 16 * (size_t)(nsplit + 1)));
+  const size_t tb = ntile * 4, b0b = blks.size() * 4;
+  DTS_TRY(g_pin_plan.ensure(512 + align256(bb) + 16 * (size_t)(nsplit + 1) + align256(tb) + b0b + 512));
   char* hp = (char*)g_pin_plan.p;
   std::memcpy(hp, &P, sizeof(P));
   std::memcpy(hp + 256, blks.data(), bb);
-  char* hs = hp + 256 + align256(bb);
+  char* htl = hp + 256 + align256(bb);
+  std::memcpy(htl, tile_blk.data(), tb);
+  std::memcpy(htl + align256(tb), blk_tile0.data(), b0b);
+  CUDA_TRY(cudaMemcpyAsync(dtile_blk, htl, tb, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(dblk_tile0, htl + align256(tb), b0b, cudaMemcpyHostToDevice, st));
+  char* hs = htl + align256(tb) + align256(b0b);
   if (nsplit) {
     std::memcpy(hs, split_keys, nsplit * sizeof(K));
     std::memcpy(hs + align256(nsplit * sizeof(K)), split_idx, nsplit * 8);
@@ -739,12 +794,13 @@ int partition_impl(const void* keys, const void* vals, uint64_t n, uint64_t gbas
   {
     using TL = ScatterTile<K, VB>;
     auto fn = k_scatter<K, VB, true>;
-    const size_t sm = scatter_layout(TL::T, TL::NT, TL::A, sizeof(K), VB, caps, true).total;
+    const size_t sm = scatter_layout(TL::T, TL::NT, sizeof(K), VB, caps, true).total;
     DTS_TRY(set_smem(fn, sm));
-    const int grid = persistent_grid(fn, TL::NT, sm, (uint32_t)blks.size());
-    fn<<<grid, TL::NT, sm, st>>>(dplan, dblks, (uint32_t)blks.size(), dctr + 1, (const K*)keys,
-                                  (const V*)vals, (K*)okeys, (V*)ovals, dscan, dsk, nullptr, dsi,
-                                  gbase, caps);
+    CUDA_TRY(cudaMemsetAsync(dstatus, 0, ntile * nbc * 4, st));
+    const int grid = persistent_grid(fn, TL::NT, sm, (uint32_t)ntile);
+    fn<<<grid, TL::NT, sm, st>>>(dplan, dblks, dtile_blk, dblk_tile0, (uint32_t)ntile, dctr + 1,
+                                  (const K*)keys, (const V*)vals, (K*)okeys, (V*)ovals, dscan,
+                                  dstatus, dsk, nullptr, dsi, gbase, caps);
     DTS_TRY(check_launch("k_scatter(split)"));
   }
   DTS_TRY(g_pin_back.ensure((G + 1) * 8 + 256));
