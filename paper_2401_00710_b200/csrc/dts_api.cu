@@ -48,7 +48,10 @@ int fail(int code, const std::string& msg) {
 // ---------------------------------------------------------------------------
 constexpr int HIST_NT = 512;
 constexpr int SAMPLE_NT = 1024;
-constexpr uint64_t BLOCK_RECORDS = 1u << 18;   // records per count-matrix row
+// scatter tile size per record width (ScatterTile<K, VB>::T) and the hist
+// block = LB consecutive tiles (one count-matrix row, look-back depth < LB)
+inline uint64_t scatter_T(int kb, int vb) { return (kb == 4 && vb <= 4) ? 512 * 9 : 512 * 5; }
+inline uint64_t block_records(int kb, int vb) { return scatter_T(kb, vb) * 8; }
 constexpr uint32_t COPY_CHUNK = 1u << 16;
 constexpr uint64_t SPAN_BATCH = 1u << 18;      // spans per k_local_sort launch
 constexpr uint64_t SAMPLE_FACTOR = 2;          // sample iff n' >= 2|S| (dtsort.py:225)
@@ -200,8 +203,13 @@ struct Bump {
 // scatter's look-back status (one u32 per tile per bucket column; tiles hold
 // >= 2560 records, columns <= 1024) — about 1.9 B per record at most.
 size_t meta_bytes(uint64_t n) {
-  const uint64_t tiles = n / 2560 + n / BLOCK_RECORDS + 2;
-  return (size_t(64) << 20) + (size_t)(n / 4) + (size_t)(tiles * 1024 * 4);
+  // (independent of the widths: 4/4 has the smallest blocks and 8/8 the
+  // smallest tiles, both bounds are used)
+  // count matrix (u32) + scan (u64) per block row and bucket column, plus the
+  // look-back status (u32 per tile and column); columns <= 1024
+  const uint64_t rows = n / block_records(4, 4) + 2;
+  const uint64_t tiles = n / 2560 + 2 * rows + 2;
+  return (size_t(64) << 20) + (size_t)(rows * 1024 * 12) + (size_t)(tiles * 1024 * 4);
 }
 
 struct HostSeg {
@@ -403,14 +411,16 @@ struct Sorter {
         hzc = std::max(hzc, (1u << g) + 1u);
         hkc = std::max(hkc, 1u << gs);
       }
-      const uint64_t rows = std::max<uint64_t>(1, (hs.len + BLOCK_RECORDS - 1) / BLOCK_RECORDS);
+      const uint64_t BR = block_records(sizeof(K), VB);
+      const uint64_t rows = std::max<uint64_t>(1, (hs.len + BR - 1) / BR);
       P.nrows = (uint32_t)rows;
       P.cnt_base = cnt_total;
       cnt_total += (uint64_t)P.nbmax * rows;
       P.bs_base = (uint32_t)bs_total;
       bs_total += P.nbmax + 1;
       nbc = std::max(nbc, P.nbmax);
-      const uint64_t per = (hs.len + rows - 1) / rows;
+      constexpr uint64_t TT = ScatterTile<K, VB>::T;  // whole tiles per block
+      const uint64_t per = ((hs.len + rows - 1) / rows + TT - 1) / TT * TT;
       for (uint64_t r = 0; r < rows; ++r) {
         Blk b;
         b.seg = (uint32_t)i;
@@ -595,7 +605,8 @@ struct Sorter {
   }
 
   size_t wave_meta_bytes(const HostSeg& s) const {
-    const uint64_t rows = std::max<uint64_t>(1, (s.len + BLOCK_RECORDS - 1) / BLOCK_RECORDS);
+    const uint64_t BR = block_records(sizeof(K), VB);
+    const uint64_t rows = std::max<uint64_t>(1, (s.len + BR - 1) / BR);
     const uint32_t g = choose_gamma(s.len, W - s.consumed);
     const uint64_t nbmax = (1u << g) + (1u << std::min(g, gs_max)) + 1u;
     const uint64_t tiles = s.len / 2560 + rows + 1;
@@ -710,7 +721,8 @@ int partition_impl(const void* keys, const void* vals, uint64_t n, uint64_t gbas
   tm.profile = false;
   tm.rep = nullptr;
   Bump meta{(char*)ws, wsb, 0};
-  const uint64_t rows = std::max<uint64_t>(1, (n + BLOCK_RECORDS - 1) / BLOCK_RECORDS);
+  const uint64_t BR = block_records(sizeof(K), VB);
+  const uint64_t rows = std::max<uint64_t>(1, (n + BR - 1) / BR);
   SegPlan P;
   std::memset(&P, 0, sizeof(P));
   P.offset = 0;
@@ -721,7 +733,8 @@ int partition_impl(const void* keys, const void* vals, uint64_t n, uint64_t gbas
   P.nheavy = (uint32_t)nsplit;
   P.nrows = (uint32_t)rows;
   std::vector<Blk> blks;
-  const uint64_t per = (n + rows - 1) / rows;
+  constexpr uint64_t TT = ScatterTile<K, VB>::T;
+  const uint64_t per = ((n + rows - 1) / rows + TT - 1) / TT * TT;
   for (uint64_t r = 0; r < rows; ++r)
     blks.push_back(Blk{0, (uint32_t)r, std::min(n, r * per), std::min(n, (r + 1) * per)});
   const uint64_t cnt_total = (uint64_t)G * rows;

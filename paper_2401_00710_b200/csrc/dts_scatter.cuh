@@ -14,6 +14,7 @@ template <typename K, int VB> struct ScatterTile {
   static constexpr int WS = 32 * IPT;  // records per warp sub-tile
   static constexpr int T = NT * IPT;
   static constexpr int NBC = 1024;     // bucket capacity (ids < 2^10)
+  static constexpr int LB = 8;         // tiles per hist block (look-back depth < LB)
 };
 
 // Decoupled look-back status word: 2-bit flag | 30-bit count (counts are
@@ -57,6 +58,10 @@ __device__ __forceinline__ uint32_t tile_body(uint64_t g0, uint32_t tn, uint32_t
   return nbody * (uint32_t)sizeof(T);
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -67,8 +72,8 @@ __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
 }
 
 // ---------------------------------------------------------------------------
-// k_scatter: persistent CTAs (2 per SM) take tiles in input order from a
-// global counter (onesweep-style).  Per tile:
+// k_scatter: persistent CTAs (2 per SM) take tiles round-robin in input
+// order (onesweep-style; the next tile is prefetched into L2).  Per tile:
 //   * keys/values arrive in SMEM by one TMA bulk copy each (cp.async.bulk on
 //     an mbarrier);
 //   * stable in-tile rank with per-warp bucket counters: warp w owns the
@@ -76,9 +81,11 @@ __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
 //     its records' ranks from SMEM atomics on its own packed u16 counters;
 //     an exclusive prefix over warps orders the warps; the in-step lane
 //     order (served by the hardware, verified here) orders the rest;
-//   * the tile's global bucket offsets come from its hist block's offsets
-//     (count matrix scan, counting.py:58-79) plus a decoupled look-back over
-//     the earlier tiles of the block (per-tile, per-bucket status words);
+//   * the tile's global bucket offsets = its hist block's offsets (count
+//     matrix scan, counting.py:58-79) + the counts of the earlier tiles of
+//     the block (< LB of them), read in parallel from per-tile status words
+//     published right after ranking (decoupled look-back, latency hidden
+//     behind the in-tile scan and regroup);
 //   * the tile is regrouped by bucket in SMEM and each bucket run is stored
 //     contiguously.  Tiles in flight are consecutive in input order, so the
 //     partial 32-byte sectors at run ends are completed by neighbouring
@@ -98,7 +105,7 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
               uint64_t global_base, Caps caps) {
   using V = typename ValOf<VB>::T;
   using TL = ScatterTile<K, VB>;
-  constexpr int NT = TL::NT, NW = TL::NW, IPT = TL::IPT, WS = TL::WS, T = TL::T;
+  constexpr int NT = TL::NT, NW = TL::NW, IPT = TL::IPT, WS = TL::WS, T = TL::T, LB = TL::LB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const ScatterLayout L = scatter_layout(T, NT, sizeof(K), VB, caps, SPLIT);
   K* skb = reinterpret_cast<K*>(smem_raw + L.sk);
@@ -111,12 +118,13 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
   uint64_t* dbase = reinterpret_cast<uint64_t*>(smem_raw + L.dbase);
   uint32_t* hz = reinterpret_cast<uint32_t*>(smem_raw + L.hz);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + L.bar);
-  __shared__ uint32_t s_t, s_fix, s_seg;
+  __shared__ uint32_t s_fix, s_seg;
   __shared__ uint32_t s_tmp[NW + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t HW = (caps.nbc + 1) / 2;  // packed counter words per warp
   const uint32_t nbs = caps.nbc;           // status row stride
   uint32_t* mywh = wh + warp * HW;
+  (void)ctr;
 
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -128,19 +136,23 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
   __syncthreads();
   uint32_t phase = 0u;
 
-  for (;;) {
-    if (tid == 0) s_t = atomicAdd(ctr, 1u);
-    __syncthreads();
-    const uint32_t t = s_t;
-    if (t >= ntile) break;
-    const uint32_t bi = tile_blk[t];
+  // tile geometry: hist block bi, tile kt within it, records [g0, g0+tn)
+  auto geom = [&](uint32_t t, uint32_t& bi, uint32_t& kt, uint64_t& g0, uint32_t& tn) {
+    bi = tile_blk[t];
     const Blk B = blks[bi];
-    const uint32_t kt = t - blk_tile0[bi];  // tile index within its hist block
+    kt = t - blk_tile0[bi];
+    g0 = B.begin + (uint64_t)kt * T;
+    tn = (uint32_t)min((uint64_t)T, B.end - g0);
+  };
+
+  for (uint32_t t = blockIdx.x; t < ntile; t += gridDim.x) {
+    uint32_t bi, kt, tn;
+    uint64_t g0;
+    geom(t, bi, kt, g0, tn);
+    const Blk B = blks[bi];
     const SegPlan P = plans[B.seg];
     const uint32_t nb = P.nb;
-    const uint64_t g0 = B.begin + (uint64_t)kt * T;
-    const uint32_t tn = (uint32_t)min((uint64_t)T, B.end - g0);
-    // ---- issue the tile loads ----
+    // ---- issue the tile loads (+ L2 prefetch of this CTA's next tile) ----
     uint32_t ko, khead, kbody, vo = 0, vhead = 0, vbody = 0;
     const uint32_t kbytes = tile_body<K>(g0, tn, ko, khead, kbody);
     uint32_t vbytes = 0;
@@ -150,6 +162,17 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
       mbar_arrive_expect_tx(&bar[0], kbytes + vbytes);
       if (kbytes) tma_load_1d(skb + ko + khead, kin + g0 + khead, kbytes, &bar[0]);
       if (vbytes) tma_load_1d(svb + vo + vhead, vin + g0 + vhead, vbytes, &bar[0]);
+      if (t + gridDim.x < ntile) {
+        uint32_t nbi, nkt, ntn, o2, h2, b2;
+        uint64_t ng0;
+        geom(t + gridDim.x, nbi, nkt, ng0, ntn);
+        const uint32_t kb2 = tile_body<K>(ng0, ntn, o2, h2, b2);
+        if (kb2) prefetch_l2(kin + ng0 + h2, kb2);
+        if (VB) {
+          const uint32_t vb2 = tile_body<V>(ng0, ntn, o2, h2, b2);
+          if (vb2) prefetch_l2(vin + ng0 + h2, vb2);
+        }
+      }
     }
     if ((uint32_t)tid < tn - kbody) {
       const uint32_t e = (uint32_t)tid < khead ? (uint32_t)tid : kbody + (uint32_t)tid;
@@ -189,8 +212,9 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
       __syncwarp();
     }
     __syncthreads();
-    // ---- per bucket: prefix over warps, tile count, look-back ----
+    // ---- per bucket pair: prefix over warps, tile counts, publish ----
     const uint32_t nw2 = (nb + 1) / 2;
+    uint32_t* myst = status + (uint64_t)t * nbs;
     for (uint32_t j = tid; j < nw2; j += NT) {
       uint32_t s = 0;
 #pragma unroll
@@ -201,32 +225,14 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
       }
       tst[2 * j] = s & 0xffffu;
       tst[2 * j + 1] = s >> 16;
-      uint32_t* my = status + (uint64_t)t * nbs + 2 * j;
-      const uint32_t fl0 = kt == 0 ? ST_INCL : ST_AGG;
-      st_volatile(my, fl0 | (s & 0xffffu));
-      if (2 * j + 1 < nb) st_volatile(my + 1, fl0 | (s >> 16));
-    }
-    __syncthreads();
-    for (uint32_t b = tid; b < nb; b += NT) {
-      const uint32_t c = tst[b];
-      uint32_t excl = 0;
-      if (kt > 0) {
-        const uint32_t* prev = status + (uint64_t)t * nbs + b;
-        for (uint32_t back = 1;; ) {
-          const uint32_t sw = ld_volatile(prev - (uint64_t)back * nbs);
-          if ((sw >> 30) == 0u) continue;  // predecessor not published yet
-          excl += sw & ST_VAL;
-          if ((sw >> 30) == 2u) break;
-          ++back;
-        }
-        st_volatile(status + (uint64_t)t * nbs + b, ST_INCL | (excl + c));
+      if (kt + 1 < LB) {  // only later tiles of the block read it
+        st_volatile(myst + 2 * j, ST_AGG | (s & 0xffffu));
+        if (2 * j + 1 < nb) st_volatile(myst + 2 * j + 1, ST_AGG | (s >> 16));
       }
-      dbase[b] = P.offset - P.scanbase + scan[P.cnt_base + (uint64_t)b * P.nrows + B.row] + excl;
     }
     __syncthreads();
     block_exscan<NT>(tst, (int)nb, s_tmp);
-    for (uint32_t b = tid; b < nb; b += NT) dbase[b] -= tst[b];
-    // ---- placement ----
+    // ---- placement (regroup by bucket in SMEM) ----
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
       if (bk[i] != 0xFFFFu) {
@@ -234,6 +240,27 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
         const uint32_t pre = (mywh[b >> 1] >> ((b & 1u) << 4)) & 0xffffu;
         const uint32_t e = warp * WS + i * 32 + lane;
         pk[tst[b] + pre + lr[i]] = (b << 16) | e;
+      }
+    }
+    // ---- global bucket bases: block offsets + earlier tiles of the block ----
+    {
+      const uint64_t* col = scan + P.cnt_base + B.row;
+      const uint64_t rb = P.offset - P.scanbase;
+      const uint32_t* st0 = status + (uint64_t)(t - kt) * nbs;
+      for (uint32_t b = tid; b < nb; b += NT) {
+        uint32_t v[LB - 1];
+#pragma unroll
+        for (int j = 0; j < LB - 1; ++j)
+          if ((uint32_t)j < kt) v[j] = ld_volatile(st0 + (uint64_t)j * nbs + b);
+        uint32_t excl = 0;
+#pragma unroll
+        for (int j = 0; j < LB - 1; ++j) {
+          if ((uint32_t)j < kt) {
+            while ((v[j] >> 30) == 0u) v[j] = ld_volatile(st0 + (uint64_t)j * nbs + b);
+            excl += v[j] & ST_VAL;
+          }
+        }
+        dbase[b] = rb + col[(uint64_t)b * P.nrows] + excl - tst[b];
       }
     }
     __syncthreads();
