@@ -154,19 +154,10 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 3)
       }
     }
     __syncthreads();
-    // ---- verify in-step order: equal digit, same warp step, rising lane ----
-    {
-      bool bad = false;
-      for (uint32_t p = tid; p + 1 < n; p += NT) {
-        const uint32_t x = si[p], y = si[p + 1];
-        const uint32_t dx = (uint32_t)(sk[p] >> sh) & (D - 1), dy = (uint32_t)(sk[p + 1] >> sh) & (D - 1);
-        bad |= dx == dy && (x >> 21) == (y >> 21) && y < x;
-      }
-      if (__any_sync(FULL, bad) && lane == 0) s_fix = 1u;
-    }
-    __syncthreads();
-    if (s_fix || DTS_FORCE_FIXUP) {
-      // general path: insertion-sort each (digit, step) group by position
+    // ---- next pass input (lane-striped) or the output; the in-step order
+    // check is fused: within one (digit, warp step) group positions must
+    // ascend.  A violation triggers the repair below and a redo. ----
+    auto group_fix = [&]() {
       for (uint32_t p = tid; p < n; p += NT) {
         const uint32_t x = si[p];
         const uint32_t dx = (uint32_t)(sk[p] >> sh) & (D - 1);
@@ -177,10 +168,10 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 3)
         if (leader && p + 1 < n && same(p + 1)) {
           uint32_t c = 2;
           while (p + c < n && same(p + c)) ++c;
-          for (uint32_t a = 1; a < c; ++a) {
-            const uint32_t xs = si[p + a];
-            const K xk = sk[p + a];
-            uint32_t b2 = a;
+          for (uint32_t a2 = 1; a2 < c; ++a2) {
+            const uint32_t xs = si[p + a2];
+            const K xk = sk[p + a2];
+            uint32_t b2 = a2;
             while (b2 > 0 && si[p + b2 - 1] > xs) {
               si[p + b2] = si[p + b2 - 1];
               sk[p + b2] = sk[p + b2 - 1];
@@ -192,23 +183,78 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 3)
         }
       }
       __syncthreads();
-      if (tid == 0) s_fix = 0u;
-    }
+    };
+    auto pair_bad = [&](K ka, uint32_t sa, K kb, uint32_t sb) {
+      return (((uint32_t)(ka >> sh) ^ (uint32_t)(kb >> sh)) & (D - 1)) == 0u &&
+             (sa >> 21) == (sb >> 21) && sb < sa;
+    };
     if (pass + 1 < npass) {
+      bool bad = false;
 #pragma unroll
       for (int i = 0; i < IPT; ++i) {
         const uint32_t e = warp * WS + i * 32 + lane;
+        K kk = k0;
+        uint32_t ss = 0xFFFFFFFFu;
         if (e < n) {
-          key[i] = sk[e];
-          idx[i] = si[e] & 0xffffu;
+          kk = sk[e];
+          ss = si[e];
+          key[i] = kk;
+          idx[i] = ss & 0xffffu;
         }
+        K kn = __shfl_down_sync(FULL, kk, 1);
+        uint32_t sn = __shfl_down_sync(FULL, ss, 1);
+        if (lane == 31 && e + 1 < n) {
+          kn = sk[e + 1];
+          sn = si[e + 1];
+        }
+        if (e + 1 < n) bad |= pair_bad(kk, ss, kn, sn);
       }
+      if (__any_sync(FULL, bad) && lane == 0) s_fix = 1u;
       __syncthreads();
+      if (s_fix || DTS_FORCE_FIXUP) {
+        group_fix();
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          const uint32_t e = warp * WS + i * 32 + lane;
+          if (e < n) {
+            key[i] = sk[e];
+            idx[i] = si[e] & 0xffffu;
+          }
+        }
+        __syncthreads();
+        if (tid == 0) s_fix = 0u;
+      }
+    } else {
+      bool bad = false;
+      for (uint32_t p0 = 0; p0 < n; p0 += NT) {
+        const uint32_t p = p0 + tid;
+        K kk = k0;
+        uint32_t ss = 0xFFFFFFFFu;
+        if (p < n) {
+          kk = sk[p];
+          ss = si[p];
+          ok[p] = kk;
+          if (VB) Av[S.offset + p] = sv[ss & 0xffffu];
+        }
+        K kn = __shfl_down_sync(FULL, kk, 1);
+        uint32_t sn = __shfl_down_sync(FULL, ss, 1);
+        if (lane == 31 && p + 1 < n) {
+          kn = sk[p + 1];
+          sn = si[p + 1];
+        }
+        if (p + 1 < n) bad |= pair_bad(kk, ss, kn, sn);
+      }
+      if (__any_sync(FULL, bad) && lane == 0) s_fix = 1u;
+      __syncthreads();
+      if (s_fix || DTS_FORCE_FIXUP) {
+        group_fix();
+        for (uint32_t p = tid; p < n; p += NT) {
+          ok[p] = sk[p];
+          if (VB) Av[S.offset + p] = sv[si[p] & 0xffffu];
+        }
+        if (tid == 0) s_fix = 0u;
+      }
     }
-  }
-  for (uint32_t i = tid; i < n; i += NT) {
-    ok[i] = sk[i];
-    if (VB) Av[S.offset + i] = sv[si[i] & 0xffffu];
   }
 }
 

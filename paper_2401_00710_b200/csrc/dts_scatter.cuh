@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
   using V = typename ValOf<VB>::T;
   using TL = ScatterTile<K, VB>;
   constexpr int NT = TL::NT, NW = TL::NW, IPT = TL::IPT, WS = TL::WS, T = TL::T, LB = TL::LB;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const ScatterLayout L = scatter_layout(T, NT, sizeof(K), VB, caps, SPLIT);
   K* skb = reinterpret_cast<K*>(smem_raw + L.sk);
   V* svb = reinterpret_cast<V*>(smem_raw + L.sv);
@@ -197,19 +197,32 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
     SR.sk = hk; SR.si = si; SR.ns = P.nheavy;
     // ---- route + per-warp rank (lane-striped within the warp sub-tile) ----
     uint32_t bk[IPT], lr[IPT];
+    auto rank_one = [&](int i, uint32_t b) {
+      const uint32_t sh = (b & 1u) << 4;
+      const uint32_t old = atomicAdd(&mywh[b >> 1], 1u << sh);
+      bk[i] = b;
+      lr[i] = (old >> sh) & 0xffffu;
+    };
+    if (!SPLIT && !(P.flags & (PF_HEAVY | PF_OVF))) {
+      // plain digit: zone = (key >> shift) & mask (sampler.py:76-88 light ids)
 #pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-      const uint32_t e = warp * WS + i * 32 + lane;
-      bk[i] = 0xFFFFu;
-      if (e < tn) {
-        const K key = sk[e];
-        const uint32_t b = SPLIT ? SR(key, global_base + g0 + e) : R(key);
-        const uint32_t sh = (b & 1u) << 4;
-        const uint32_t old = atomicAdd(&mywh[b >> 1], 1u << sh);
-        bk[i] = b;
-        lr[i] = (old >> sh) & 0xffffu;
+      for (int i = 0; i < IPT; ++i) {
+        const uint32_t e = warp * WS + i * 32 + lane;
+        bk[i] = 0xFFFFu;
+        if (e < tn) rank_one(i, (uint32_t)(sk[e] >> R.shift) & R.mask);
+        __syncwarp();
       }
-      __syncwarp();
+    } else {
+#pragma unroll
+      for (int i = 0; i < IPT; ++i) {
+        const uint32_t e = warp * WS + i * 32 + lane;
+        bk[i] = 0xFFFFu;
+        if (e < tn) {
+          const K key = sk[e];
+          rank_one(i, SPLIT ? SR(key, global_base + g0 + e) : R(key));
+        }
+        __syncwarp();
+      }
     }
     __syncthreads();
     // ---- per bucket pair: prefix over warps, tile counts, publish ----
@@ -264,16 +277,27 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
       }
     }
     __syncthreads();
-    // ---- verify the in-step order (see dts_rank.cuh); zero the counters ----
+    // ---- write the bucket runs; the in-step order check (dts_rank.cuh) is
+    // fused here: pairs (p, p+1) of one group must ascend.  If a pair does
+    // not, the groups are re-sorted and the whole tile is written again
+    // (same addresses, corrected values).  Counters are zeroed meanwhile. ----
     for (uint32_t i = tid; i < NW * HW; i += NT) wh[i] = 0u;
-    {
-      bool bad = false;
-      for (uint32_t p = tid; p + 1 < tn; p += NT) {
-        const uint32_t x = pk[p], y = pk[p + 1];
-        bad |= ((x ^ y) < 32u) && (y < x);  // same bucket & step, descending
+    bool bad = false;
+#pragma unroll
+    for (int it = 0; it < IPT; ++it) {
+      const uint32_t p = it * NT + tid;
+      const uint32_t wd = p < tn ? pk[p] : 0xFFFFFFFFu;
+      uint32_t nx = __shfl_down_sync(FULL, wd, 1);
+      if (lane == 31) nx = p + 1 < tn ? pk[p + 1] : 0xFFFFFFFFu;
+      bad |= ((wd ^ nx) < 32u) && (nx < wd);
+      if (p < tn) {
+        const uint32_t bb = wd >> 16, e = wd & 0xffffu;
+        const uint64_t d = dbase[bb] + p;
+        kout[d] = sk[e];
+        if (VB) vout[d] = sv[e];
       }
-      if (__any_sync(FULL, bad) && lane == 0) s_fix = 1u;
     }
+    if (__any_sync(FULL, bad) && lane == 0) s_fix = 1u;
     __syncthreads();
     if (s_fix || DTS_FORCE_FIXUP) {
       for (uint32_t p = tid; p < tn; p += NT) {
@@ -286,19 +310,14 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
         }
       }
       __syncthreads();
-      if (tid == 0) s_fix = 0u;
-    }
-    // ---- write the bucket runs ----
-#pragma unroll
-    for (int it = 0; it < IPT; ++it) {
-      const uint32_t p = it * NT + tid;
-      if (p < tn) {
+      for (uint32_t p = tid; p < tn; p += NT) {
         const uint32_t wd = pk[p];
-        const uint32_t b = wd >> 16, e = wd & 0xffffu;
-        const uint64_t d = dbase[b] + p;
+        const uint32_t bb = wd >> 16, e = wd & 0xffffu;
+        const uint64_t d = dbase[bb] + p;
         kout[d] = sk[e];
         if (VB) vout[d] = sv[e];
       }
+      if (tid == 0) s_fix = 0u;
     }
     __syncthreads();
   }
