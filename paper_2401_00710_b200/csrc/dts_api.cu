@@ -537,12 +537,11 @@ struct Sorter {
       tm.begin(DTS_K_SCATTER, ev);
       using TL = ScatterTile<K, VB>;
       auto fn = k_scatter<K, VB, false>;
-      const size_t sm = scatter_layout(TL::T, TL::NT, sizeof(K), VB, caps, false).total;
+      const size_t sm = ScatterSmem<K, VB, false>::total;
       DTS_TRY(set_smem(fn, sm));
       const int grid = persistent_grid(fn, TL::NT, sm, (uint32_t)ntile);
-      fn<<<grid, TL::NT, sm, st>>>(dplans, dblks, dtile_blk, dblk_tile0, (uint32_t)ntile,
-                                    dctr + 1, ink, inv, outk, outv, dscan, dstatus, dheavy, dhz,
-                                    nullptr, 0, caps);
+      fn<<<grid, TL::NT, sm, st>>>(dplans, dblks, dtile_blk, dblk_tile0, (uint32_t)ntile, nbc,
+                                    ink, inv, outk, outv, dscan, dstatus, dheavy, dhz, nullptr, 0);
       tm.end(ev, wave_recs);
       DTS_TRY(check_launch("k_scatter"));
     }
@@ -807,13 +806,13 @@ int partition_impl(const void* keys, const void* vals, uint64_t n, uint64_t gbas
   {
     using TL = ScatterTile<K, VB>;
     auto fn = k_scatter<K, VB, true>;
-    const size_t sm = scatter_layout(TL::T, TL::NT, sizeof(K), VB, caps, true).total;
+    const size_t sm = ScatterSmem<K, VB, true>::total;
     DTS_TRY(set_smem(fn, sm));
     CUDA_TRY(cudaMemsetAsync(dstatus, 0, ntile * nbc * 4, st));
     const int grid = persistent_grid(fn, TL::NT, sm, (uint32_t)ntile);
-    fn<<<grid, TL::NT, sm, st>>>(dplan, dblks, dtile_blk, dblk_tile0, (uint32_t)ntile, dctr + 1,
+    fn<<<grid, TL::NT, sm, st>>>(dplan, dblks, dtile_blk, dblk_tile0, (uint32_t)ntile, nbc,
                                   (const K*)keys, (const V*)vals, (K*)okeys, (V*)ovals, dscan,
-                                  dstatus, dsk, nullptr, dsi, gbase, caps);
+                                  dstatus, dsk, nullptr, dsi, gbase);
     DTS_TRY(check_launch("k_scatter(split)"));
   }
   DTS_TRY(g_pin_back.ensure((G + 1) * 8 + 256));

@@ -15,6 +15,8 @@ template <typename K, int VB> struct ScatterTile {
   static constexpr int T = NT * IPT;
   static constexpr int NBC = 1024;     // bucket capacity (ids < 2^10)
   static constexpr int LB = 8;         // tiles per hist block (look-back depth < LB)
+  static constexpr int HKC = 1024;     // heavy keys / splitters capacity
+  static constexpr int HZC = 520;      // zone table capacity (2^9 + 1, padded)
 };
 
 // Decoupled look-back status word: 2-bit flag | 30-bit count (counts are
@@ -23,27 +25,25 @@ constexpr uint32_t ST_AGG = 1u << 30;
 constexpr uint32_t ST_INCL = 2u << 30;
 constexpr uint32_t ST_VAL = (1u << 30) - 1u;
 
-struct ScatterLayout {
-  size_t sk, sv, hk, si, pk, wh, tst, dbase, hz, bar, total;
+__host__ __device__ constexpr size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// Compile-time SMEM layout (immediate-offset addressing in the kernel).
+template <typename K, int VB, bool SPLIT> struct ScatterSmem {
+  using TL = ScatterTile<K, VB>;
+  static constexpr size_t sk = 0;
+  static constexpr size_t sv = a16(sk + (size_t)(TL::T + 8) * sizeof(K));
+  static constexpr size_t pk = a16(sv + (size_t)(TL::T + 8) * VB);
+  static constexpr size_t wh = a16(pk + (size_t)TL::T * 4);
+  static constexpr size_t tst = a16(wh + (size_t)TL::NW * (TL::NBC / 2) * 4);
+  static constexpr size_t db = a16(tst + (size_t)(TL::NBC + 1) * 4);
+  static constexpr size_t hk = a16(db + (size_t)TL::NBC * 4);
+  static constexpr size_t si = a16(hk + (size_t)(SPLIT ? TL::HKC : 256) * sizeof(K));
+  static constexpr size_t hz = a16(si + (SPLIT ? (size_t)TL::HKC * 8 : 0));
+  static constexpr size_t geo = a16(hz + (SPLIT ? 0 : (size_t)TL::HZC * 4));
+  static constexpr size_t plan = a16(geo + 2 * 32);
+  static constexpr size_t bar = a16(plan + 2 * sizeof(SegPlan));
+  static constexpr size_t total = a16(bar + 16);
 };
-__host__ __device__ inline ScatterLayout scatter_layout(int T, int NT, int kb, int vb, Caps c,
-                                                        bool split) {
-  ScatterLayout L;
-  size_t o = 0;
-  const size_t nb = c.nbc;
-  L.sk = o; o = align16(o + (size_t)(T + 8) * kb);
-  L.sv = o; o = align16(o + (size_t)(T + 8) * vb);
-  L.hk = o; o = align16(o + (size_t)c.hkc * kb);
-  L.si = o; o = align16(o + (split ? (size_t)c.hkc * 8 : 0));
-  L.pk = o; o = align16(o + (size_t)T * 4);
-  L.wh = o; o = align16(o + (size_t)(NT / 32) * ((nb + 1) / 2) * 4);
-  L.tst = o; o = align16(o + (nb + 1) * 4);
-  L.dbase = o; o = align16(o + nb * 8);
-  L.hz = o; o = align16(o + (size_t)c.hzc * 4);
-  L.bar = o; o = align16(o + 16);
-  L.total = o;
-  return L;
-}
 
 // Split [g0, g0+tn) of a T-typed column into head / 16-byte aligned body /
 // tail; returns the body bytes (moved by cp.async.bulk).
@@ -61,7 +61,6 @@ __device__ __forceinline__ uint32_t tile_body(uint64_t g0, uint32_t tn, uint32_t
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
-
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -71,60 +70,89 @@ __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
   asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+struct TileGeo {  // one scatter tile: hist block bi, tile kt in it, records [g0, g0+tn)
+  uint64_t g0;
+  uint32_t tn, kt, bi, seg, row, t;
+};
+
 // ---------------------------------------------------------------------------
 // k_scatter: persistent CTAs (2 per SM) take tiles round-robin in input
-// order (onesweep-style; the next tile is prefetched into L2).  Per tile:
+// order (onesweep-style).  Per tile:
 //   * keys/values arrive in SMEM by one TMA bulk copy each (cp.async.bulk on
-//     an mbarrier);
+//     an mbarrier); warp 1 meanwhile resolves the CTA's next tile and
+//     prefetches it into L2;
 //   * stable in-tile rank with per-warp bucket counters: warp w owns the
 //     contiguous sub-tile [w*WS, (w+1)*WS) in lane-striped order and takes
 //     its records' ranks from SMEM atomics on its own packed u16 counters;
 //     an exclusive prefix over warps orders the warps; the in-step lane
 //     order (served by the hardware, verified here) orders the rest;
-//   * the tile's global bucket offsets = its hist block's offsets (count
-//     matrix scan, counting.py:58-79) + the counts of the earlier tiles of
-//     the block (< LB of them), read in parallel from per-tile status words
-//     published right after ranking (decoupled look-back, latency hidden
-//     behind the in-tile scan and regroup);
+//   * the tile's bucket bases = its hist block's offsets (count matrix scan,
+//     counting.py:58-79, loaded early) + the counts of the earlier tiles of
+//     the block (< LB of them, read in parallel from per-tile status words
+//     published right after ranking: decoupled look-back);
 //   * the tile is regrouped by bucket in SMEM and each bucket run is stored
 //     contiguously.  Tiles in flight are consecutive in input order, so the
 //     partial 32-byte sectors at run ends are completed by neighbouring
-//     tiles within microseconds and merge in L2 (no partial-sector traffic).
+//     tiles within microseconds and merge in L2.
 // Stable for every block and tile count (counting.py:1-10 invariant;
 // scatter_block, _kernels.py:12-25, keeps the same per-bucket `run` order).
+// Segment-relative positions are u32 (segments < 2^32 records).
 // ---------------------------------------------------------------------------
 template <typename K, int VB, bool SPLIT>
 __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
     k_scatter(const SegPlan* __restrict__ plans, const Blk* __restrict__ blks,
               const uint32_t* __restrict__ tile_blk, const uint32_t* __restrict__ blk_tile0,
-              uint32_t ntile, uint32_t* __restrict__ ctr, const K* __restrict__ kin,
+              uint32_t ntile, uint32_t nbs, const K* __restrict__ kin,
               const typename ValOf<VB>::T* __restrict__ vin, K* __restrict__ kout,
               typename ValOf<VB>::T* __restrict__ vout, const uint64_t* __restrict__ scan,
               uint32_t* __restrict__ status, const K* __restrict__ heavy_pool,
               const uint32_t* __restrict__ hz_pool, const uint64_t* __restrict__ split_idx,
-              uint64_t global_base, Caps caps) {
+              uint64_t global_base) {
   using V = typename ValOf<VB>::T;
   using TL = ScatterTile<K, VB>;
+  using SL = ScatterSmem<K, VB, SPLIT>;
   constexpr int NT = TL::NT, NW = TL::NW, IPT = TL::IPT, WS = TL::WS, T = TL::T, LB = TL::LB;
+  constexpr uint32_t HW = TL::NBC / 2;  // packed counter words per warp
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const ScatterLayout L = scatter_layout(T, NT, sizeof(K), VB, caps, SPLIT);
-  K* skb = reinterpret_cast<K*>(smem_raw + L.sk);
-  V* svb = reinterpret_cast<V*>(smem_raw + L.sv);
-  K* hk = reinterpret_cast<K*>(smem_raw + L.hk);
-  uint64_t* si = reinterpret_cast<uint64_t*>(smem_raw + L.si);
-  uint32_t* pk = reinterpret_cast<uint32_t*>(smem_raw + L.pk);
-  uint32_t* wh = reinterpret_cast<uint32_t*>(smem_raw + L.wh);
-  uint32_t* tst = reinterpret_cast<uint32_t*>(smem_raw + L.tst);
-  uint64_t* dbase = reinterpret_cast<uint64_t*>(smem_raw + L.dbase);
-  uint32_t* hz = reinterpret_cast<uint32_t*>(smem_raw + L.hz);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + L.bar);
+  K* skb = reinterpret_cast<K*>(smem_raw + SL::sk);
+  V* svb = reinterpret_cast<V*>(smem_raw + SL::sv);
+  uint32_t* pk = reinterpret_cast<uint32_t*>(smem_raw + SL::pk);
+  uint32_t* wh = reinterpret_cast<uint32_t*>(smem_raw + SL::wh);
+  uint32_t* tst = reinterpret_cast<uint32_t*>(smem_raw + SL::tst);
+  uint32_t* db = reinterpret_cast<uint32_t*>(smem_raw + SL::db);
+  K* hk = reinterpret_cast<K*>(smem_raw + SL::hk);
+  uint64_t* si = reinterpret_cast<uint64_t*>(smem_raw + SL::si);
+  uint32_t* hz = reinterpret_cast<uint32_t*>(smem_raw + SL::hz);
+  TileGeo* sgeo = reinterpret_cast<TileGeo*>(smem_raw + SL::geo);
+  SegPlan* splan = reinterpret_cast<SegPlan*>(smem_raw + SL::plan);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + SL::bar);
   __shared__ uint32_t s_fix, s_seg;
   __shared__ uint32_t s_tmp[NW + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t HW = (caps.nbc + 1) / 2;  // packed counter words per warp
-  const uint32_t nbs = caps.nbc;           // status row stride
   uint32_t* mywh = wh + warp * HW;
-  (void)ctr;
+
+  // resolve tile t's geometry and plan into slot `slot` (one warp)
+  auto resolve = [&](uint32_t t, int slot) {
+    if (lane == 0) {
+      const uint32_t bi = tile_blk[t];
+      const Blk B = blks[bi];
+      TileGeo g;
+      g.kt = t - blk_tile0[bi];
+      g.g0 = B.begin + (uint64_t)g.kt * T;
+      g.tn = (uint32_t)min((uint64_t)T, B.end - g.g0);
+      g.bi = bi;
+      g.seg = B.seg;
+      g.row = B.row;
+      g.t = t;
+      sgeo[slot] = g;
+    }
+    __syncwarp();
+    const uint32_t seg = sgeo[slot].seg;
+    constexpr int PW = sizeof(SegPlan) / 4;
+    if (lane < PW)
+      reinterpret_cast<uint32_t*>(&splan[slot])[lane] =
+          reinterpret_cast<const uint32_t*>(&plans[seg])[lane];
+  };
 
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -133,26 +161,17 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
     s_seg = 0xFFFFFFFFu;
   }
   for (uint32_t i = tid; i < NW * HW; i += NT) wh[i] = 0u;
+  if (warp == 0 && blockIdx.x < ntile) resolve(blockIdx.x, 0);
   __syncthreads();
   uint32_t phase = 0u;
+  int cur = 0;
 
-  // tile geometry: hist block bi, tile kt within it, records [g0, g0+tn)
-  auto geom = [&](uint32_t t, uint32_t& bi, uint32_t& kt, uint64_t& g0, uint32_t& tn) {
-    bi = tile_blk[t];
-    const Blk B = blks[bi];
-    kt = t - blk_tile0[bi];
-    g0 = B.begin + (uint64_t)kt * T;
-    tn = (uint32_t)min((uint64_t)T, B.end - g0);
-  };
-
-  for (uint32_t t = blockIdx.x; t < ntile; t += gridDim.x) {
-    uint32_t bi, kt, tn;
-    uint64_t g0;
-    geom(t, bi, kt, g0, tn);
-    const Blk B = blks[bi];
-    const SegPlan P = plans[B.seg];
-    const uint32_t nb = P.nb;
-    // ---- issue the tile loads (+ L2 prefetch of this CTA's next tile) ----
+  for (uint32_t t = blockIdx.x; t < ntile; t += gridDim.x, cur ^= 1) {
+    const TileGeo G = sgeo[cur];
+    const SegPlan& P = splan[cur];
+    const uint32_t nb = P.nb, tn = G.tn, kt = G.kt;
+    const uint64_t g0 = G.g0;
+    // ---- issue the tile loads ----
     uint32_t ko, khead, kbody, vo = 0, vhead = 0, vbody = 0;
     const uint32_t kbytes = tile_body<K>(g0, tn, ko, khead, kbody);
     uint32_t vbytes = 0;
@@ -162,17 +181,6 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
       mbar_arrive_expect_tx(&bar[0], kbytes + vbytes);
       if (kbytes) tma_load_1d(skb + ko + khead, kin + g0 + khead, kbytes, &bar[0]);
       if (vbytes) tma_load_1d(svb + vo + vhead, vin + g0 + vhead, vbytes, &bar[0]);
-      if (t + gridDim.x < ntile) {
-        uint32_t nbi, nkt, ntn, o2, h2, b2;
-        uint64_t ng0;
-        geom(t + gridDim.x, nbi, nkt, ng0, ntn);
-        const uint32_t kb2 = tile_body<K>(ng0, ntn, o2, h2, b2);
-        if (kb2) prefetch_l2(kin + ng0 + h2, kb2);
-        if (VB) {
-          const uint32_t vb2 = tile_body<V>(ng0, ntn, o2, h2, b2);
-          if (vb2) prefetch_l2(vin + ng0 + h2, vb2);
-        }
-      }
     }
     if ((uint32_t)tid < tn - kbody) {
       const uint32_t e = (uint32_t)tid < khead ? (uint32_t)tid : kbody + (uint32_t)tid;
@@ -183,18 +191,37 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
       const uint32_t e = t2 < vhead ? t2 : vbody + t2;
       svb[vo + e] = vin[g0 + e];
     }
-    if (B.seg != s_seg) {  // block-uniform
+    // hist-block offsets of this tile's buckets (needed much later)
+    uint32_t boff[TL::NBC / NT];
+#pragma unroll
+    for (int r = 0; r < TL::NBC / NT; ++r) {
+      const uint32_t b = tid + r * NT;
+      boff[r] = b < nb ? (uint32_t)(scan[P.cnt_base + (uint64_t)b * P.nrows + G.row] - P.scanbase)
+                       : 0u;
+    }
+    if (G.seg != s_seg) {  // block-uniform
       load_tables<K>(P, heavy_pool, hz_pool, split_idx, hk, si, hz);
     }
+    // next tile: geometry + plan into the other slot, data into L2
+    if (warp == 1 && t + gridDim.x < ntile) {
+      resolve(t + gridDim.x, cur ^ 1);
+      if (lane == 0) {
+        const TileGeo& N = sgeo[cur ^ 1];
+        uint32_t o2, h2, b2;
+        const uint32_t kb2 = tile_body<K>(N.g0, N.tn, o2, h2, b2);
+        if (kb2) prefetch_l2(kin + N.g0 + h2, kb2);
+        if (VB) {
+          const uint32_t vb2 = tile_body<V>(N.g0, N.tn, o2, h2, b2);
+          if (vb2) prefetch_l2(vin + N.g0 + h2, vb2);
+        }
+      }
+    }
     __syncthreads();
-    if (tid == 0) s_seg = B.seg;
+    if (tid == 0) s_seg = G.seg;
     mbar_wait(&bar[0], phase);
     phase ^= 1u;
     const K* sk = skb + ko;
     const V* sv = svb + vo;
-    const Router<K> R = make_router<K>(P, hz, hk);
-    SplitRouter<K> SR;
-    SR.sk = hk; SR.si = si; SR.ns = P.nheavy;
     // ---- route + per-warp rank (lane-striped within the warp sub-tile) ----
     uint32_t bk[IPT], lr[IPT];
     auto rank_one = [&](int i, uint32_t b) {
@@ -203,16 +230,29 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
       bk[i] = b;
       lr[i] = (old >> sh) & 0xffffu;
     };
+    const bool full = tn == (uint32_t)T;
     if (!SPLIT && !(P.flags & (PF_HEAVY | PF_OVF))) {
       // plain digit: zone = (key >> shift) & mask (sampler.py:76-88 light ids)
+      const uint32_t shift = P.shift, mask = (1u << P.gamma) - 1u;
+      if (full) {
 #pragma unroll
-      for (int i = 0; i < IPT; ++i) {
-        const uint32_t e = warp * WS + i * 32 + lane;
-        bk[i] = 0xFFFFu;
-        if (e < tn) rank_one(i, (uint32_t)(sk[e] >> R.shift) & R.mask);
-        __syncwarp();
+        for (int i = 0; i < IPT; ++i) {
+          rank_one(i, (uint32_t)(sk[warp * WS + i * 32 + lane] >> shift) & mask);
+          __syncwarp();
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          const uint32_t e = warp * WS + i * 32 + lane;
+          bk[i] = 0xFFFFu;
+          if (e < tn) rank_one(i, (uint32_t)(sk[e] >> shift) & mask);
+          __syncwarp();
+        }
       }
     } else {
+      const Router<K> R = make_router<K>(P, hz, hk);
+      SplitRouter<K> SR;
+      SR.sk = hk; SR.si = si; SR.ns = P.nheavy;
 #pragma unroll
       for (int i = 0; i < IPT; ++i) {
         const uint32_t e = warp * WS + i * 32 + lane;
@@ -226,9 +266,8 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
     }
     __syncthreads();
     // ---- per bucket pair: prefix over warps, tile counts, publish ----
-    const uint32_t nw2 = (nb + 1) / 2;
     uint32_t* myst = status + (uint64_t)t * nbs;
-    for (uint32_t j = tid; j < nw2; j += NT) {
+    for (uint32_t j = tid; j < (nb + 1) / 2; j += NT) {
       uint32_t s = 0;
 #pragma unroll
       for (int w = 0; w < NW; ++w) {
@@ -246,55 +285,69 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
     __syncthreads();
     block_exscan<NT>(tst, (int)nb, s_tmp);
     // ---- placement (regroup by bucket in SMEM) ----
+    if (full) {
 #pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-      if (bk[i] != 0xFFFFu) {
+      for (int i = 0; i < IPT; ++i) {
         const uint32_t b = bk[i];
         const uint32_t pre = (mywh[b >> 1] >> ((b & 1u) << 4)) & 0xffffu;
-        const uint32_t e = warp * WS + i * 32 + lane;
-        pk[tst[b] + pre + lr[i]] = (b << 16) | e;
+        pk[tst[b] + pre + lr[i]] = (b << 16) | (warp * WS + i * 32 + lane);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < IPT; ++i) {
+        if (bk[i] != 0xFFFFu) {
+          const uint32_t b = bk[i];
+          const uint32_t pre = (mywh[b >> 1] >> ((b & 1u) << 4)) & 0xffffu;
+          pk[tst[b] + pre + lr[i]] = (b << 16) | (warp * WS + i * 32 + lane);
+        }
       }
     }
-    // ---- global bucket bases: block offsets + earlier tiles of the block ----
+    // each warp read only its own counters above: reset them for the next tile
+    __syncwarp();
+    for (uint32_t i = lane; i < HW; i += 32) mywh[i] = 0u;
+    // ---- bucket bases: block offsets + earlier tiles of the block ----
     {
-      const uint64_t* col = scan + P.cnt_base + B.row;
-      const uint64_t rb = P.offset - P.scanbase;
       const uint32_t* st0 = status + (uint64_t)(t - kt) * nbs;
-      for (uint32_t b = tid; b < nb; b += NT) {
-        uint32_t v[LB - 1];
 #pragma unroll
-        for (int j = 0; j < LB - 1; ++j)
-          if ((uint32_t)j < kt) v[j] = ld_volatile(st0 + (uint64_t)j * nbs + b);
-        uint32_t excl = 0;
+      for (int r = 0; r < TL::NBC / NT; ++r) {
+        const uint32_t b = tid + r * NT;
+        if (b < nb) {
+          uint32_t v[LB - 1];
 #pragma unroll
-        for (int j = 0; j < LB - 1; ++j) {
-          if ((uint32_t)j < kt) {
-            while ((v[j] >> 30) == 0u) v[j] = ld_volatile(st0 + (uint64_t)j * nbs + b);
-            excl += v[j] & ST_VAL;
+          for (int j = 0; j < LB - 1; ++j)
+            if ((uint32_t)j < kt) v[j] = ld_volatile(st0 + (uint64_t)j * nbs + b);
+          uint32_t excl = 0;
+#pragma unroll
+          for (int j = 0; j < LB - 1; ++j) {
+            if ((uint32_t)j < kt) {
+              while ((v[j] >> 30) == 0u) v[j] = ld_volatile(st0 + (uint64_t)j * nbs + b);
+              excl += v[j] & ST_VAL;
+            }
           }
+          db[b] = boff[r] + excl - tst[b];
         }
-        dbase[b] = rb + col[(uint64_t)b * P.nrows] + excl - tst[b];
       }
     }
     __syncthreads();
     // ---- write the bucket runs; the in-step order check (dts_rank.cuh) is
-    // fused here: pairs (p, p+1) of one group must ascend.  If a pair does
-    // not, the groups are re-sorted and the whole tile is written again
-    // (same addresses, corrected values).  Counters are zeroed meanwhile. ----
-    for (uint32_t i = tid; i < NW * HW; i += NT) wh[i] = 0u;
+    // fused: pairs (p, p+1) of one group must ascend.  If a pair does not,
+    // the groups are re-sorted and the tile is written again (same
+    // addresses, corrected values). ----
+    K* ko_seg = kout + P.offset;
+    V* vo_seg = VB ? vout + P.offset : nullptr;
     bool bad = false;
 #pragma unroll
     for (int it = 0; it < IPT; ++it) {
       const uint32_t p = it * NT + tid;
-      const uint32_t wd = p < tn ? pk[p] : 0xFFFFFFFFu;
+      const uint32_t wd = (full || p < tn) ? pk[p] : 0xFFFFFFFFu;
       uint32_t nx = __shfl_down_sync(FULL, wd, 1);
       if (lane == 31) nx = p + 1 < tn ? pk[p + 1] : 0xFFFFFFFFu;
       bad |= ((wd ^ nx) < 32u) && (nx < wd);
-      if (p < tn) {
+      if (full || p < tn) {
         const uint32_t bb = wd >> 16, e = wd & 0xffffu;
-        const uint64_t d = dbase[bb] + p;
-        kout[d] = sk[e];
-        if (VB) vout[d] = sv[e];
+        const uint32_t d = db[bb] + p;
+        ko_seg[d] = sk[e];
+        if (VB) vo_seg[d] = sv[e];
       }
     }
     if (__any_sync(FULL, bad) && lane == 0) s_fix = 1u;
@@ -313,13 +366,13 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
       for (uint32_t p = tid; p < tn; p += NT) {
         const uint32_t wd = pk[p];
         const uint32_t bb = wd >> 16, e = wd & 0xffffu;
-        const uint64_t d = dbase[bb] + p;
-        kout[d] = sk[e];
-        if (VB) vout[d] = sv[e];
+        const uint32_t d = db[bb] + p;
+        ko_seg[d] = sk[e];
+        if (VB) vo_seg[d] = sv[e];
       }
+      __syncthreads();
       if (tid == 0) s_fix = 0u;
     }
-    __syncthreads();
   }
 }
 
