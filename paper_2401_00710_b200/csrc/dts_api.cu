@@ -9,6 +9,7 @@
 // plan the next one.  Output is the unique stable sort, identical to the
 // reference's.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -61,6 +62,17 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v ? std::atoi(v) : dflt;
+}
+
+// DTS_TRACE=1: one stderr line per wave (host planning / wait / classify µs)
+inline double now_us() {
+  return std::chrono::duration<double, std::micro>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+inline bool trace_on() {
+  static const int t = env_int("DTS_TRACE", 0);
+  return t != 0;
 }
 
 // Local-sort capacity per record width (SMEM ~ CAP*(kb+vb+2) bytes).
@@ -371,6 +383,7 @@ struct Sorter {
                std::vector<HostSeg>& next) {
     const size_t ns = s1 - s0;
     const bool dt = cfg.mode == DTS_MODE_DT;
+    const double t_plan0 = trace_on() ? now_us() : 0.0;
     // ---- host plans ----
     std::vector<SegPlan> plans(ns);
     std::vector<Blk> blks;
@@ -546,6 +559,7 @@ struct Sorter {
       DTS_TRY(check_launch("k_scatter"));
     }
     // ---- read back ----
+    const double t_launch = trace_on() ? now_us() : 0.0;
     DTS_TRY(g_pin_back.ensure(align256(pb) + align256(bs_total * 8) + bs_total + 256));
     char* bp = (char*)g_pin_back.p;
     CUDA_TRY(cudaMemcpyAsync(bp, dplans, pb, cudaMemcpyDeviceToHost, st));
@@ -553,6 +567,7 @@ struct Sorter {
     CUDA_TRY(cudaMemcpyAsync(bp + align256(pb) + align256(bs_total * 8), dkinds, bs_total,
                              cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    const double t_sync = trace_on() ? now_us() : 0.0;
     tm.harvest();
     meta.off = save;
     const SegPlan* rp = (const SegPlan*)bp;
@@ -599,6 +614,18 @@ struct Sorter {
           next.push_back(HostSeg{lo, sz, (uint32_t)W - rem, false});
         }
       }
+    }
+    if (trace_on()) {
+      const double t_cls = now_us();
+      const size_t nsp = spans.size() + (have_cur ? 1 : 0), ncp = copies.size();
+      const int rc = launch_spans_and_copies();
+      std::fprintf(stderr,
+                   "[dts] level %d segs %zu recs %llu blks %zu tiles %llu sampled %zu | plan+launch %.0f us, "
+                   "gpu wait %.0f us, classify %.0f us, spans %zu copies %zu next %zu, span launch %.0f us\n",
+                   level, ns, (unsigned long long)wave_recs, blks.size(), (unsigned long long)ntile,
+                   sampled.size(), t_launch - t_plan0, t_sync - t_launch, t_cls - t_sync, nsp, ncp,
+                   next.size(), now_us() - t_cls);
+      return rc;
     }
     return launch_spans_and_copies();
   }
