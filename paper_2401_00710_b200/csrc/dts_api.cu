@@ -346,11 +346,11 @@ struct Sorter {
       Timer::Ev ev;
       tm.begin(DTS_K_LOCAL, ev);
       {
-        using LT = LocalTile<K, VB>;
         auto fn = k_local_sort<K, VB>;
-        const size_t sm = local_layout(LT::CAP, LT::NT, sizeof(K), VB, LT::RB).total;
+        const size_t sm = LocalSmem<K, VB>::total;
         DTS_TRY(set_smem(fn, sm));
-        fn<<<(unsigned)cnt, LT::NT, sm, st>>>(dsp, Ak, Av, Tk, Tv);
+        const int grid = persistent_grid(fn, LocalTile<K, VB>::NT, sm, (uint32_t)cnt);
+        fn<<<grid, LocalTile<K, VB>::NT, sm, st>>>(dsp, (uint32_t)cnt, Ak, Av, Tk, Tv);
       }
       tm.end(ev, recs);
       DTS_TRY(check_launch("k_local_sort"));
@@ -475,7 +475,7 @@ struct Sorter {
     uint32_t* dctr = (uint32_t*)meta.take(16);
     uint32_t* dtile_blk = (uint32_t*)meta.take(std::max<uint64_t>(1, ntile) * 4);
     uint32_t* dblk_tile0 = (uint32_t*)meta.take(std::max<size_t>(1, blks.size()) * 4);
-    uint32_t* dstatus = (uint32_t*)meta.take(std::max<uint64_t>(1, ntile) * nbc * 4);
+    uint32_t* dstatus = (uint32_t*)meta.take(std::max<uint64_t>(1, ntile) * (nbc / 2) * 4);
     if (!dplans || !dblks || !dsampled || !dcnt || !dscan || !dpart || !dbs || !dkinds ||
         !dheavy || !dhz || !dctr || !dtile_blk || !dblk_tile0 || !dstatus)
       return fail(DTS_ENOMEM, "workspace too small for level metadata");
@@ -545,7 +545,7 @@ struct Sorter {
     // ---- scatter ----
     {
       CUDA_TRY(cudaMemsetAsync(dctr + 1, 0, 4, st));
-      CUDA_TRY(cudaMemsetAsync(dstatus, 0, ntile * nbc * 4, st));
+      CUDA_TRY(cudaMemsetAsync(dstatus, 0, ntile * (nbc / 2) * 4, st));
       Timer::Ev ev;
       tm.begin(DTS_K_SCATTER, ev);
       using TL = ScatterTile<K, VB>;
@@ -553,7 +553,7 @@ struct Sorter {
       const size_t sm = ScatterSmem<K, VB, false>::total;
       DTS_TRY(set_smem(fn, sm));
       const int grid = persistent_grid(fn, TL::NT, sm, (uint32_t)ntile);
-      fn<<<grid, TL::NT, sm, st>>>(dplans, dblks, dtile_blk, dblk_tile0, (uint32_t)ntile, nbc,
+      fn<<<grid, TL::NT, sm, st>>>(dplans, dblks, dtile_blk, dblk_tile0, (uint32_t)ntile, nbc / 2,
                                     ink, inv, outk, outv, dscan, dstatus, dheavy, dhz, nullptr, 0);
       tm.end(ev, wave_recs);
       DTS_TRY(check_launch("k_scatter"));
@@ -789,7 +789,7 @@ int partition_impl(const void* keys, const void* vals, uint64_t n, uint64_t gbas
   const uint32_t nbc = (G + 1) & ~1u;
   uint32_t* dtile_blk = (uint32_t*)meta.take(std::max<uint64_t>(1, ntile) * 4);
   uint32_t* dblk_tile0 = (uint32_t*)meta.take(std::max<size_t>(1, blks.size()) * 4);
-  uint32_t* dstatus = (uint32_t*)meta.take(std::max<uint64_t>(1, ntile) * nbc * 4);
+  uint32_t* dstatus = (uint32_t*)meta.take(std::max<uint64_t>(1, ntile) * (nbc / 2) * 4);
   if (!dplan || !dblks || !dcnt || !dscan || !dpart || !dbs || !dkinds || !dsk || !dsi || !dctr ||
       !dtile_blk || !dblk_tile0 || !dstatus)
     return fail(DTS_ENOMEM, "workspace too small for partition metadata");
@@ -835,9 +835,9 @@ int partition_impl(const void* keys, const void* vals, uint64_t n, uint64_t gbas
     auto fn = k_scatter<K, VB, true>;
     const size_t sm = ScatterSmem<K, VB, true>::total;
     DTS_TRY(set_smem(fn, sm));
-    CUDA_TRY(cudaMemsetAsync(dstatus, 0, ntile * nbc * 4, st));
+    CUDA_TRY(cudaMemsetAsync(dstatus, 0, ntile * (nbc / 2) * 4, st));
     const int grid = persistent_grid(fn, TL::NT, sm, (uint32_t)ntile);
-    fn<<<grid, TL::NT, sm, st>>>(dplan, dblks, dtile_blk, dblk_tile0, (uint32_t)ntile, nbc,
+    fn<<<grid, TL::NT, sm, st>>>(dplan, dblks, dtile_blk, dblk_tile0, (uint32_t)ntile, nbc / 2,
                                   (const K*)keys, (const V*)vals, (K*)okeys, (V*)ovals, dscan,
                                   dstatus, dsk, nullptr, dsi, gbase);
     DTS_TRY(check_launch("k_scatter(split)"));
@@ -1038,6 +1038,26 @@ bool valid_widths(int kb, int vb) { return (kb == 4 || kb == 8) && (vb == 0 || v
 // C ABI
 // ===========================================================================
 extern "C" {
+
+// Tools-only: per-phase cycle sums of k_scatter (DTS_PHASE_PROF builds);
+// returns the number of entries written (0 in product builds).
+int dts_debug_phases(unsigned long long* out, int n, int reset) {
+#if DTS_PHASE_PROF
+  unsigned long long h[16];
+  if (cudaMemcpyFromSymbol(h, g_phase, sizeof(h)) != cudaSuccess) return -1;
+  const int m = n < 16 ? n : 16;
+  for (int i = 0; i < m; ++i) out[i] = h[i];
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+  }
+  return m;
+#else
+  (void)out; (void)n; (void)reset;
+  return 0;
+#endif
+}
+
 
 size_t dts_workspace_bytes(uint64_t n, int key_bytes, int val_bytes) {
   if (!valid_widths(key_bytes, val_bytes)) return 0;

@@ -1,218 +1,361 @@
 // dts_local.cuh — k_local_sort, the base case (dtsort.py:127-147 _base_sort:
 // stable sort by full key of a span of adjacent buckets, valid per :128-131).
 #pragma once
-#include "dts_rank.cuh"
-#include "dts_sort_kernels.cuh"
+#include "dts_scatter.cuh"
 
 namespace dts {
 
 template <typename K, int VB> struct LocalTile {
-  static constexpr int NT = 256;
+  static constexpr int NT = 512;
   static constexpr int NW = NT / 32;
-  static constexpr int IPT = 17;
+  static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? 9 : 5;
   static constexpr int WS = 32 * IPT;  // records per warp sub-tile
-  static constexpr int CAP = NT * IPT;
-  static constexpr int RB = 8;         // radix bits per pass (<= 2^8 digit values)
+  static constexpr int CAP = NT * IPT; // records per span
+  static constexpr int RB = 8;         // LSD radix bits per pass (fallback path)
+  static constexpr int CB = 13;        // counting path: spans differing in <= CB bits
+  static constexpr int FIXMAX = 64;    // counting path: largest equal-key group
 };
 
-struct LocalLayout {
-  size_t sk, sv, si, wc, dt, total;
+// Compile-time SMEM layout: two span buffers (TMA double buffering), the
+// per-record index array, and the counter area (8192 packed u16 bins for the
+// counting path; per-warp digit counters + digit totals for the LSD path).
+template <typename K, int VB> struct LocalSmem {
+  using TL = LocalTile<K, VB>;
+  static constexpr size_t kcap = (size_t)(TL::CAP + 8) * sizeof(K);
+  static constexpr size_t vcap = (size_t)(TL::CAP + 8) * VB;
+  static constexpr size_t k0 = 0;
+  static constexpr size_t v0 = a16(k0 + kcap);
+  static constexpr size_t k1 = a16(v0 + vcap);
+  static constexpr size_t v1 = a16(k1 + kcap);
+  static constexpr size_t si = a16(v1 + vcap);
+  static constexpr size_t cnt = a16(si + (size_t)TL::CAP * 4);
+  static constexpr size_t cnt_bytes = ((size_t)1 << TL::CB) * 2;
+  static constexpr size_t wc_bytes = (size_t)TL::NW * ((size_t)1 << (TL::RB - 1)) * 4;
+  static_assert(wc_bytes + (((size_t)1 << TL::RB) + 1) * 4 <= cnt_bytes, "LSD counters alias cnt");
+  static constexpr size_t bar = a16(cnt + cnt_bytes);
+  static constexpr size_t total = a16(bar + 16);
 };
-__host__ __device__ inline LocalLayout local_layout(int CAP, int NT, int kb, int vb, int RB) {
-  LocalLayout L;
-  size_t o = 0;
-  L.sk = o; o = align16(o + (size_t)(CAP + 8) * kb);
-  L.sv = o; o = align16(o + (size_t)(CAP + 8) * vb);
-  L.si = o; o = align16(o + (size_t)CAP * 4);
-  L.wc = o; o = align16(o + (size_t)(NT / 32) * ((size_t)1 << (RB - 1)) * 4);
-  L.dt = o; o = align16(o + (((size_t)1 << RB) + 1) * 4);
-  L.total = o;
-  return L;
-}
+
+struct SpanSlot {  // a span staged in one buffer
+  uint64_t offset;
+  uint32_t len, src, ko, vo;
+};
 
 // ---------------------------------------------------------------------------
-// k_local_sort: one CTA per span (<= CAP records).  Loads the span into SMEM,
-// finds the bits that differ inside it (keys agree above bit `bits`), and
-// runs stable LSD passes of <= RB bits.  Each pass ranks records with the
-// per-warp counter scheme of k_scatter (warp w owns a contiguous sub-tile in
-// lane-striped order; SMEM atomics on its packed u16 digit counters; an
-// exclusive prefix over (digit, warp)); in-step order is verified and
-// repaired if ever needed.  Records move as (key, position|slot) pairs;
-// payloads are gathered once at the end.  Output always lands in A.
+// k_local_sort: persistent CTAs (2 per SM) take spans round-robin; while one
+// span is sorted the next one is already streaming into the other SMEM
+// buffer (one cp.async.bulk per column on its mbarrier).  Per span:
+//   * the bits in which its keys differ (keys agree above `bits`);
+//   * bits <= CB (the common case: last-level buckets): ONE counting pass on
+//     the differing bits — those bits are the whole key order — SMEM-atomic
+//     histogram, scan, atomic slots, then each equal-key group (<= FIXMAX
+//     records, else the LSD path) is put back in input order (insertion sort
+//     of record indices): stable without relying on any atomic ordering;
+//   * otherwise stable LSD passes of <= RB bits with per-warp packed counters
+//     (the k_scatter ranking; in-step order verified and repaired if needed).
+// Output always lands in A.
 // ---------------------------------------------------------------------------
 template <typename K, int VB>
-__global__ void __launch_bounds__(LocalTile<K, VB>::NT, 3)
-    k_local_sort(const Span* __restrict__ spans, K* __restrict__ Ak,
+__global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
+    k_local_sort(const Span* __restrict__ spans, uint32_t nspan, K* __restrict__ Ak,
                  typename ValOf<VB>::T* __restrict__ Av, const K* __restrict__ Tk,
                  const typename ValOf<VB>::T* __restrict__ Tv) {
   using V = typename ValOf<VB>::T;
   using TL = LocalTile<K, VB>;
-  constexpr int NT = TL::NT, NW = TL::NW, IPT = TL::IPT, WS = TL::WS, CAP = TL::CAP;
+  using SL = LocalSmem<K, VB>;
+  constexpr int NT = TL::NT, NW = TL::NW, IPT = TL::IPT, WS = TL::WS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const LocalLayout L = local_layout(CAP, NT, sizeof(K), VB, TL::RB);
-  K* skb = reinterpret_cast<K*>(smem_raw + L.sk);
-  V* svb = reinterpret_cast<V*>(smem_raw + L.sv);
-  uint32_t* si = reinterpret_cast<uint32_t*>(smem_raw + L.si);
-  uint32_t* wc = reinterpret_cast<uint32_t*>(smem_raw + L.wc);
-  uint32_t* dt = reinterpret_cast<uint32_t*>(smem_raw + L.dt);
-  __shared__ uint32_t s_tmp[NW + 1];
+  uint32_t* si = reinterpret_cast<uint32_t*>(smem_raw + SL::si);
+  uint16_t* si16 = reinterpret_cast<uint16_t*>(smem_raw + SL::si);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw + SL::cnt);
+  uint32_t* wc = cnt;
+  uint32_t* dt = reinterpret_cast<uint32_t*>(smem_raw + SL::cnt + SL::wc_bytes);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + SL::bar);
+  __shared__ SpanSlot s_slot[2];
+  __shared__ uint32_t s_wt[NW + 1];
   __shared__ K s_diff[NW];
-  __shared__ uint32_t s_fix;
+  __shared__ uint32_t s_fix, s_big;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  const Span S = spans[blockIdx.x];
-  const uint32_t n = S.len;
-  const K* srck = S.src ? Tk : Ak;
-  const V* srcv = S.src ? Tv : Av;
-  const uint32_t ko = stage_tile<K, NT>(skb, srck, S.offset, n);
-  uint32_t vo = 0;
-  if (VB) vo = stage_tile<V, NT>(svb, srcv, S.offset, n);
-  K* sk = skb + ko;
-  const V* sv = svb + vo;
-  if (tid == 0) s_fix = 0u;
-  __syncthreads();
-  const K k0 = sk[0];
-  K key[IPT];
-  uint32_t idx[IPT];
-  K diff = 0;
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const uint32_t e = warp * WS + i * 32 + lane;
-    key[i] = e < n ? sk[e] : k0;
-    idx[i] = e;
-    diff |= key[i] ^ k0;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) diff |= __shfl_xor_sync(FULL, diff, o);
-  if (lane == 0) s_diff[warp] = diff;
-  __syncthreads();
-  diff = 0;
-#pragma unroll
-  for (int w = 0; w < NW; ++w) diff |= s_diff[w];
-  int bits = 0;
-  if (diff) bits = (sizeof(K) == 8) ? 64 - __clzll((long long)diff) : 32 - __clz((int)(uint32_t)diff);
+  // issue span `s` into buffer `b` (thread 0; the descriptor is in hand)
+  auto issue = [&](const Span& S, int b) {
+    const K* kc = S.src ? Tk : Ak;
+    const V* vc = S.src ? Tv : Av;
+    SpanSlot sl;
+    sl.offset = S.offset;
+    sl.len = S.len;
+    sl.src = S.src;
+    const char* ks;
+    const uint32_t kbytes = S.len ? tile_span<K>(kc, S.offset, S.len, ks, sl.ko) : 0u;
+    const char* vs = nullptr;
+    uint32_t vbytes = 0;
+    sl.vo = 0;
+    if (VB && S.len) vbytes = tile_span<V>(vc, S.offset, S.len, vs, sl.vo);
+    s_slot[b] = sl;
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&bar[b], kbytes + vbytes);
+    if (kbytes) tma_load_1d(smem_raw + (b ? SL::k1 : SL::k0), ks, kbytes, &bar[b]);
+    if (vbytes) tma_load_1d(smem_raw + (b ? SL::v1 : SL::v0), vs, vbytes, &bar[b]);
+  };
 
-  K* ok = Ak + S.offset;
-  if (bits == 0) {
-    if (S.src) {
-      for (uint32_t i = tid; i < n; i += NT) {
-        ok[i] = sk[i];
-        if (VB) Av[S.offset + i] = sv[i];
-      }
+  const uint32_t G = gridDim.x;
+  Span nextS;  // thread 0: descriptor of the span after the one in flight
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    s_fix = 0u;
+    s_big = 0u;
+    if (blockIdx.x < nspan) issue(spans[blockIdx.x], 0);
+    if (blockIdx.x + G < nspan) nextS = spans[blockIdx.x + G];
+  }
+  __syncthreads();
+  uint32_t ph0 = 0u, ph1 = 0u;
+  int cur = 0;
+  for (uint32_t sidx = blockIdx.x; sidx < nspan; sidx += G, cur ^= 1) {
+    // stream the next span into the other buffer (freed by the previous
+    // iteration's final barrier); fetch the descriptor after it
+    if (tid == 0) {
+      if (sidx + G < nspan) issue(nextS, cur ^ 1);
+      if (sidx + 2 * G < nspan) nextS = spans[sidx + 2 * G];
     }
-    return;
-  }
+    if (cur == 0) {
+      mbar_wait(&bar[0], ph0);
+      ph0 ^= 1u;
+    } else {
+      mbar_wait(&bar[1], ph1);
+      ph1 ^= 1u;
+    }
+    const SpanSlot S = s_slot[cur];
+    const uint32_t n = S.len;
+    K* sk = reinterpret_cast<K*>(smem_raw + (cur ? SL::k1 : SL::k0)) + S.ko;
+    V* sv = reinterpret_cast<V*>(smem_raw + (cur ? SL::v1 : SL::v0)) + S.vo;
+    K* ok = Ak + S.offset;
+    V* ov = VB ? Av + S.offset : nullptr;
 
-  const int npass = (bits + TL::RB - 1) / TL::RB;
-  const int pb = (bits + npass - 1) / npass;
-  uint32_t* mywc = wc + warp * (1u << (TL::RB - 1));
-  for (int pass = 0; pass < npass; ++pass) {
-    const int sh = pass * pb;
-    const int pbits = min(pb, bits - sh);
-    const uint32_t D = 1u << pbits;
-    const uint32_t DW = (D + 1) / 2;  // packed counter words per warp
-    for (uint32_t i = tid; i < NW * (1u << (TL::RB - 1)); i += NT) wc[i] = 0u;
-    __syncthreads();
-    // ---- per-warp rank: lane-striped steps, atomics on own counters ----
-    uint32_t dg[IPT], lr[IPT];
+    // ---- keys into registers (lane-striped warp sub-tiles), differing bits ----
+    const K k0 = sk[0];
+    K key[IPT];
+    K diff = 0;
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
       const uint32_t e = warp * WS + i * 32 + lane;
-      if (e < n) {
-        const uint32_t d = (uint32_t)(key[i] >> sh) & (D - 1);
-        const uint32_t s2 = (d & 1u) << 4;
-        const uint32_t old = atomicAdd(&mywc[d >> 1], 1u << s2);
-        dg[i] = d;
-        lr[i] = (old >> s2) & 0xffffu;
-      }
-      __syncwarp();
+      key[i] = e < n ? sk[e] : k0;
+      diff |= key[i] ^ k0;
     }
-    __syncthreads();
-    // ---- exclusive prefix over warps per digit, digit totals ----
-    for (uint32_t j = tid; j < DW; j += NT) {
-      uint32_t s = 0;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const uint32_t x = wc[w * (1u << (TL::RB - 1)) + j];
-        wc[w * (1u << (TL::RB - 1)) + j] = s;
-        s += x;
-      }
-      dt[2 * j] = s & 0xffffu;
-      dt[2 * j + 1] = s >> 16;
-    }
+    for (int o = 16; o > 0; o >>= 1) diff |= __shfl_xor_sync(FULL, diff, o);
+    if (lane == 0) s_diff[warp] = diff;
+    if (tid == 0) s_big = 0u;  // read only after the scan barrier below
     __syncthreads();
-    block_exscan<NT>(dt, (int)D, s_tmp);
-    // ---- placement (all records are in registers) ----
+    diff = 0;
 #pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-      const uint32_t e = warp * WS + i * 32 + lane;
-      if (e < n) {
-        const uint32_t d = dg[i];
-        const uint32_t pos = dt[d] + ((mywc[d >> 1] >> ((d & 1u) << 4)) & 0xffffu) + lr[i];
-        sk[pos] = key[i];
-        si[pos] = (e << 16) | idx[i];
-      }
-    }
-    __syncthreads();
-    // ---- next pass input (lane-striped) or the output; the in-step order
-    // check is fused: within one (digit, warp step) group positions must
-    // ascend.  A violation triggers the repair below and a redo. ----
-    auto group_fix = [&]() {
-      for (uint32_t p = tid; p < n; p += NT) {
-        const uint32_t x = si[p];
-        const uint32_t dx = (uint32_t)(sk[p] >> sh) & (D - 1);
-        auto same = [&](uint32_t q) {
-          return ((uint32_t)(sk[q] >> sh) & (D - 1)) == dx && (si[q] >> 21) == (x >> 21);
-        };
-        const bool leader = p == 0 || !same(p - 1);
-        if (leader && p + 1 < n && same(p + 1)) {
-          uint32_t c = 2;
-          while (p + c < n && same(p + c)) ++c;
-          for (uint32_t a2 = 1; a2 < c; ++a2) {
-            const uint32_t xs = si[p + a2];
-            const K xk = sk[p + a2];
-            uint32_t b2 = a2;
-            while (b2 > 0 && si[p + b2 - 1] > xs) {
-              si[p + b2] = si[p + b2 - 1];
-              sk[p + b2] = sk[p + b2 - 1];
-              --b2;
-            }
-            si[p + b2] = xs;
-            sk[p + b2] = xk;
-          }
+    for (int w = 0; w < NW; ++w) diff |= s_diff[w];
+    int bits = 0;
+    if (diff) bits = (sizeof(K) == 8) ? 64 - __clzll((long long)diff) : 32 - __clz((int)(uint32_t)diff);
+
+    if (bits == 0) {
+      if (S.src) {
+        for (uint32_t i = tid; i < n; i += NT) {
+          ok[i] = sk[i];
+          if (VB) ov[i] = sv[i];
         }
       }
       __syncthreads();
-    };
-    auto pair_bad = [&](K ka, uint32_t sa, K kb, uint32_t sb) {
-      return (((uint32_t)(ka >> sh) ^ (uint32_t)(kb >> sh)) & (D - 1)) == 0u &&
-             (sa >> 21) == (sb >> 21) && sb < sa;
-    };
-    if (pass + 1 < npass) {
-      bool bad = false;
+      continue;
+    }
+
+    bool lsd = bits > TL::CB;
+    if (!lsd) {
+      // ================= counting path: one pass on the differing bits ==========
+      const uint32_t nbin = 1u << bits, mask = nbin - 1u, nwd = (nbin + 1) >> 1;
+      for (uint32_t i = tid; i < nwd; i += NT) cnt[i] = 0u;
+      __syncthreads();
 #pragma unroll
       for (int i = 0; i < IPT; ++i) {
         const uint32_t e = warp * WS + i * 32 + lane;
-        K kk = k0;
-        uint32_t ss = 0xFFFFFFFFu;
         if (e < n) {
-          kk = sk[e];
-          ss = si[e];
-          key[i] = kk;
-          idx[i] = ss & 0xffffu;
+          const uint32_t d = (uint32_t)key[i] & mask;
+          atomicAdd(&cnt[d >> 1], 1u << ((d & 1u) << 4));
         }
-        K kn = __shfl_down_sync(FULL, kk, 1);
-        uint32_t sn = __shfl_down_sync(FULL, ss, 1);
-        if (lane == 31 && e + 1 < n) {
-          kn = sk[e + 1];
-          sn = si[e + 1];
+      }
+      __syncthreads();
+      // exclusive scan over the bins (thread-contiguous word ranges), and the
+      // largest group
+      const uint32_t wpt = (nwd + NT - 1) / NT;
+      const uint32_t w0 = min(nwd, tid * wpt), w1 = min(nwd, w0 + wpt);
+      uint32_t sum = 0, mx = 0;
+      for (uint32_t w = w0; w < w1; ++w) {
+        const uint32_t x = cnt[w];
+        sum += (x & 0xffffu) + (x >> 16);
+        mx = max(mx, max(x & 0xffffu, x >> 16));
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+      if (lane == 31) s_wt[warp] = incl;
+      if (lane == 0 && mx > (uint32_t)TL::FIXMAX) s_big = 1u;
+      __syncthreads();
+      uint32_t wp = lane < NW ? s_wt[lane] : 0u;
+#pragma unroll
+      for (int o = 1; o < NW; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, wp, o);
+        if (lane >= o) wp += y;
+      }
+      const uint32_t wex = __shfl_sync(FULL, wp, (warp + 31) & 31);
+      uint32_t base = (warp ? wex : 0u) + incl - sum;
+      for (uint32_t w = w0; w < w1; ++w) {
+        const uint32_t x = cnt[w];
+        const uint32_t lo = x & 0xffffu;
+        cnt[w] = base | ((base + lo) << 16);
+        base += lo + (x >> 16);
+      }
+      __syncthreads();
+      lsd = s_big != 0u;
+      if (!lsd) {
+        // atomic slots (arbitrary order inside a group of equal keys)
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          const uint32_t e = warp * WS + i * 32 + lane;
+          if (e < n) {
+            const uint32_t d = (uint32_t)key[i] & mask;
+            const uint32_t sh = (d & 1u) << 4;
+            const uint32_t old = atomicAdd(&cnt[d >> 1], 1u << sh);
+            si16[(old >> sh) & 0xffffu] = (uint16_t)e;
+          }
         }
-        if (e + 1 < n) bad |= pair_bad(kk, ss, kn, sn);
+        __syncthreads();
+        // each group of equal keys back into input order
+        const uint32_t bpt = (nbin + NT - 1) / NT;
+        const uint32_t d0 = min(nbin, tid * bpt), d1 = min(nbin, d0 + bpt);
+        uint32_t start = 0;
+        if (d0 > 0 && d0 < d1) {
+          const uint32_t dp = d0 - 1;
+          start = (cnt[dp >> 1] >> ((dp & 1u) << 4)) & 0xffffu;
+        }
+        for (uint32_t d = d0; d < d1; ++d) {
+          const uint32_t end = (cnt[d >> 1] >> ((d & 1u) << 4)) & 0xffffu;
+          if (end - start >= 2u) {
+            for (uint32_t a = start + 1; a < end; ++a) {
+              const uint16_t x = si16[a];
+              uint32_t b = a;
+              while (b > start && si16[b - 1] > x) {
+                si16[b] = si16[b - 1];
+                --b;
+              }
+              si16[b] = x;
+            }
+          }
+          start = end;
+        }
+        __syncthreads();
+        for (uint32_t p = tid; p < n; p += NT) {
+          const uint32_t e = si16[p];
+          ok[p] = sk[e];
+          if (VB) ov[p] = sv[e];
+        }
+        __syncthreads();
+        continue;
+      }
+    }
+
+    // ================= LSD path: stable passes of <= RB bits ==================
+    uint32_t idx[IPT];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) idx[i] = warp * WS + i * 32 + lane;
+    const int npass = (bits + TL::RB - 1) / TL::RB;
+    const int pb = (bits + npass - 1) / npass;
+    uint32_t* mywc = wc + warp * (1u << (TL::RB - 1));
+    for (int pass = 0; pass < npass; ++pass) {
+      const int sh = pass * pb;
+      const int pbits = min(pb, bits - sh);
+      const uint32_t D = 1u << pbits;
+      const uint32_t DW = (D + 1) / 2;  // packed counter words per warp
+      for (uint32_t i = tid; i < NW * (1u << (TL::RB - 1)); i += NT) wc[i] = 0u;
+      __syncthreads();
+      uint32_t dg[IPT], lr[IPT];
+#pragma unroll
+      for (int i = 0; i < IPT; ++i) {
+        const uint32_t e = warp * WS + i * 32 + lane;
+        if (e < n) {
+          const uint32_t d = (uint32_t)(key[i] >> sh) & (D - 1);
+          const uint32_t s2 = (d & 1u) << 4;
+          const uint32_t old = atomicAdd(&mywc[d >> 1], 1u << s2);
+          dg[i] = d;
+          lr[i] = (old >> s2) & 0xffffu;
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      for (uint32_t j = tid; j < DW; j += NT) {
+        uint32_t s = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const uint32_t x = wc[w * (1u << (TL::RB - 1)) + j];
+          wc[w * (1u << (TL::RB - 1)) + j] = s;
+          s += x;
+        }
+        dt[2 * j] = s & 0xffffu;
+        dt[2 * j + 1] = s >> 16;
+      }
+      __syncthreads();
+      block_exscan<NT>(dt, (int)D, s_wt);
+#pragma unroll
+      for (int i = 0; i < IPT; ++i) {
+        const uint32_t e = warp * WS + i * 32 + lane;
+        if (e < n) {
+          const uint32_t d = dg[i];
+          const uint32_t pos = dt[d] + ((mywc[d >> 1] >> ((d & 1u) << 4)) & 0xffffu) + lr[i];
+          sk[pos] = key[i];
+          si[pos] = (e << 16) | idx[i];
+        }
+      }
+      __syncthreads();
+      // in-step order check: within one (digit, warp step) group positions
+      // must ascend; a violation is repaired by re-sorting the groups
+      bool bad = false;
+      for (uint32_t p = tid; p + 1 < n; p += NT) {
+        const uint32_t a = si[p], b = si[p + 1];
+        const bool same = ((((uint32_t)(sk[p] >> sh) ^ (uint32_t)(sk[p + 1] >> sh)) & (D - 1)) == 0u) &&
+                          ((a >> 21) == (b >> 21));
+        bad |= same && b < a;
       }
       if (__any_sync(FULL, bad) && lane == 0) s_fix = 1u;
       __syncthreads();
       if (s_fix || DTS_FORCE_FIXUP) {
-        group_fix();
+        for (uint32_t p = tid; p < n; p += NT) {
+          const uint32_t x = si[p];
+          const uint32_t dx = (uint32_t)(sk[p] >> sh) & (D - 1);
+          auto same = [&](uint32_t q) {
+            return ((uint32_t)(sk[q] >> sh) & (D - 1)) == dx && (si[q] >> 21) == (x >> 21);
+          };
+          const bool leader = p == 0 || !same(p - 1);
+          if (leader && p + 1 < n && same(p + 1)) {
+            uint32_t c = 2;
+            while (p + c < n && same(p + c)) ++c;
+            for (uint32_t a2 = 1; a2 < c; ++a2) {
+              const uint32_t xs = si[p + a2];
+              const K xk = sk[p + a2];
+              uint32_t b2 = a2;
+              while (b2 > 0 && si[p + b2 - 1] > xs) {
+                si[p + b2] = si[p + b2 - 1];
+                sk[p + b2] = sk[p + b2 - 1];
+                --b2;
+              }
+              si[p + b2] = xs;
+              sk[p + b2] = xk;
+            }
+          }
+        }
+        __syncthreads();
+        if (tid == 0) s_fix = 0u;
+      }
+      if (pass + 1 < npass) {
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
           const uint32_t e = warp * WS + i * 32 + lane;
@@ -222,39 +365,13 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 3)
           }
         }
         __syncthreads();
-        if (tid == 0) s_fix = 0u;
-      }
-    } else {
-      bool bad = false;
-      for (uint32_t p0 = 0; p0 < n; p0 += NT) {
-        const uint32_t p = p0 + tid;
-        K kk = k0;
-        uint32_t ss = 0xFFFFFFFFu;
-        if (p < n) {
-          kk = sk[p];
-          ss = si[p];
-          ok[p] = kk;
-          if (VB) Av[S.offset + p] = sv[ss & 0xffffu];
-        }
-        K kn = __shfl_down_sync(FULL, kk, 1);
-        uint32_t sn = __shfl_down_sync(FULL, ss, 1);
-        if (lane == 31 && p + 1 < n) {
-          kn = sk[p + 1];
-          sn = si[p + 1];
-        }
-        if (p + 1 < n) bad |= pair_bad(kk, ss, kn, sn);
-      }
-      if (__any_sync(FULL, bad) && lane == 0) s_fix = 1u;
-      __syncthreads();
-      if (s_fix || DTS_FORCE_FIXUP) {
-        group_fix();
-        for (uint32_t p = tid; p < n; p += NT) {
-          ok[p] = sk[p];
-          if (VB) Av[S.offset + p] = sv[si[p] & 0xffffu];
-        }
-        if (tid == 0) s_fix = 0u;
       }
     }
+    for (uint32_t p = tid; p < n; p += NT) {
+      ok[p] = sk[p];
+      if (VB) ov[p] = sv[si[p] & 0xffffu];
+    }
+    __syncthreads();
   }
 }
 

@@ -19,11 +19,12 @@ template <typename K, int VB> struct ScatterTile {
   static constexpr int HZC = 520;      // zone table capacity (2^9 + 1, padded)
 };
 
-// Decoupled look-back status word: 2-bit flag | 30-bit count (counts are
-// relative to the hist block, which is < 2^30 records).
-constexpr uint32_t ST_AGG = 1u << 30;
-constexpr uint32_t ST_INCL = 2u << 30;
-constexpr uint32_t ST_VAL = (1u << 30) - 1u;
+// Look-back status: one u32 per (tile, bucket pair) = the tile's packed
+// counts of buckets 2j (bits 0-12) and 2j+1 (bits 16-28) | ST_VALID (bit 15).
+// Tile counts are <= T < 2^13 and a tile sums <= LB-1 predecessors, so the
+// packed sums never carry into bit 15 or bit 31.
+constexpr uint32_t ST_VALID = 0x8000u;
+constexpr uint32_t ST_MASK = 0x7fff7fffu;
 
 __host__ __device__ constexpr size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -33,7 +34,7 @@ template <typename K, int VB, bool SPLIT> struct ScatterSmem {
   static constexpr size_t sk = 0;
   static constexpr size_t sv = a16(sk + (size_t)(TL::T + 8) * sizeof(K));
   static constexpr size_t pk = a16(sv + (size_t)(TL::T + 8) * VB);
-  static constexpr size_t wh = a16(pk + (size_t)TL::T * 4);
+  static constexpr size_t wh = a16(pk + (size_t)(TL::T + 1) * 4);  // + sentinel
   static constexpr size_t tst = a16(wh + (size_t)TL::NW * (TL::NBC / 2) * 4);
   static constexpr size_t db = a16(tst + (size_t)(TL::NBC + 1) * 4);
   static constexpr size_t hk = a16(db + (size_t)TL::NBC * 4);
@@ -58,6 +59,20 @@ __device__ __forceinline__ uint32_t tile_body(uint64_t g0, uint32_t tn, uint32_t
   return nbody * (uint32_t)sizeof(T);
 }
 
+// 16-byte aligned superset [floor16(g0), ceil16(g0+tn)) of a column's tile
+// (whole 16-byte chunks never cross a page, so the few extra bytes read at
+// either end are always mapped); `off` = elements before g0 in SMEM.
+template <typename T>
+__device__ __forceinline__ uint32_t tile_span(const T* col, uint64_t g0, uint32_t tn,
+                                              const char*& src, uint32_t& off) {
+  const uint64_t b0 = reinterpret_cast<uint64_t>(col + g0);
+  const uint64_t a0 = b0 & ~uint64_t(15);
+  const uint64_t a1 = (reinterpret_cast<uint64_t>(col + g0 + tn) + 15) & ~uint64_t(15);
+  src = reinterpret_cast<const char*>(a0);
+  off = (uint32_t)(b0 - a0) / (uint32_t)sizeof(T);
+  return (uint32_t)(a1 - a0);
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
@@ -69,6 +84,53 @@ __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
 __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
   asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+
+__device__ __forceinline__ void st_global(uint32_t* p, uint32_t v) {
+  asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v));
+}
+__device__ __forceinline__ void st_global(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.global.u64 [%0], %1;" ::"l"(p), "l"(v));
+}
+__device__ __forceinline__ void st_global(unsigned long* p, unsigned long v) {
+  asm volatile("st.global.u64 [%0], %1;" ::"l"(p), "l"(v));
+}
+template <typename T>
+__device__ __forceinline__ T* opaque_ptr(T* p) {
+  asm volatile("mov.b64 %0, %0;" : "+l"(p));
+  return p;
+}
+
+// DTS_PHASE_PROF=1 (tools build only): thread 0 of every CTA accumulates
+// clock64() cycles per tile phase; read back with dts_debug_phases().
+// DTS_SCATTER_EXP (experiment builds only, results are WRONG): bit 0 drops
+// the global stores of the write-out, bit 1 drops the look-back waits.
+#ifndef DTS_SCATTER_EXP
+#define DTS_SCATTER_EXP 0
+#endif
+#ifndef DTS_PHASE_PROF
+#define DTS_PHASE_PROF 0
+#endif
+#if DTS_PHASE_PROF
+__device__ unsigned long long g_phase[16];
+#define PH_INIT unsigned long long ph_acc[10] = {0}; long long ph_t = clock64();
+#define PH(k)                                  \
+  if (tid == 0) {                              \
+    const long long now_ = clock64();          \
+    ph_acc[k] += (unsigned long long)(now_ - ph_t); \
+    ph_t = now_;                               \
+  }
+#define PH_SPIN if (tid < 512) atomicAdd(&g_phase[15], 1ull);
+#define PH_DONE                                                        \
+  if (tid == 0) {                                                      \
+    for (int k_ = 0; k_ < 10; ++k_) atomicAdd(&g_phase[k_], ph_acc[k_]); \
+    atomicAdd(&g_phase[14], 1ull);                                     \
+  }
+#else
+#define PH_INIT
+#define PH(k)
+#define PH_SPIN
+#define PH_DONE
+#endif
 
 struct TileGeo {  // one scatter tile: hist block bi, tile kt in it, records [g0, g0+tn)
   uint64_t g0;
@@ -112,7 +174,9 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
   using TL = ScatterTile<K, VB>;
   using SL = ScatterSmem<K, VB, SPLIT>;
   constexpr int NT = TL::NT, NW = TL::NW, IPT = TL::IPT, WS = TL::WS, T = TL::T, LB = TL::LB;
-  constexpr uint32_t HW = TL::NBC / 2;  // packed counter words per warp
+  constexpr uint32_t HW = TL::NBC / 2;  // packed counter words per warp = bucket pairs
+  static_assert(HW <= (uint32_t)NT, "one bucket pair per thread");
+  static_assert((LB - 1) * T < 32768 && T < 8192, "packed look-back sums must not carry");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K* skb = reinterpret_cast<K*>(smem_raw + SL::sk);
   V* svb = reinterpret_cast<V*>(smem_raw + SL::sv);
@@ -127,7 +191,7 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
   SegPlan* splan = reinterpret_cast<SegPlan*>(smem_raw + SL::plan);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + SL::bar);
   __shared__ uint32_t s_fix, s_seg;
-  __shared__ uint32_t s_tmp[NW + 1];
+  __shared__ uint32_t s_wt[NW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t* mywh = wh + warp * HW;
 
@@ -159,69 +223,60 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
     fence_mbar_init();
     s_fix = 0u;
     s_seg = 0xFFFFFFFFu;
+    pk[T] = 0xFFFFFFFFu;  // write-out sentinel of full tiles
   }
   for (uint32_t i = tid; i < NW * HW; i += NT) wh[i] = 0u;
   if (warp == 0 && blockIdx.x < ntile) resolve(blockIdx.x, 0);
   __syncthreads();
   uint32_t phase = 0u;
   int cur = 0;
+  PH_INIT
 
   for (uint32_t t = blockIdx.x; t < ntile; t += gridDim.x, cur ^= 1) {
+    PH(0)
     const TileGeo G = sgeo[cur];
     const SegPlan& P = splan[cur];
     const uint32_t nb = P.nb, tn = G.tn, kt = G.kt;
+    const uint32_t npair = (nb + 1) >> 1;
     const uint64_t g0 = G.g0;
-    // ---- issue the tile loads ----
-    uint32_t ko, khead, kbody, vo = 0, vhead = 0, vbody = 0;
-    const uint32_t kbytes = tile_body<K>(g0, tn, ko, khead, kbody);
-    uint32_t vbytes = 0;
-    if (VB) vbytes = tile_body<V>(g0, tn, vo, vhead, vbody);
-    if (tid == 0) {
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&bar[0], kbytes + vbytes);
-      if (kbytes) tma_load_1d(skb + ko + khead, kin + g0 + khead, kbytes, &bar[0]);
-      if (vbytes) tma_load_1d(svb + vo + vhead, vin + g0 + vhead, vbytes, &bar[0]);
+    const bool full = tn == (uint32_t)T;
+    // ---- issue the tile loads (one bulk copy per column) ----
+    uint32_t ko, vo = 0;
+    {
+      const char* ksrc;
+      const uint32_t kbytes = tile_span<K>(kin, g0, tn, ksrc, ko);
+      const char* vsrc = nullptr;
+      uint32_t vbytes = 0;
+      if (VB) vbytes = tile_span<V>(vin, g0, tn, vsrc, vo);
+      if (tid == 0) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bar[0], kbytes + vbytes);
+        tma_load_1d(skb, ksrc, kbytes, &bar[0]);
+        if (VB) tma_load_1d(svb, vsrc, vbytes, &bar[0]);
+        if (!full) pk[tn] = 0xFFFFFFFFu;  // sentinel
+      }
     }
-    if ((uint32_t)tid < tn - kbody) {
-      const uint32_t e = (uint32_t)tid < khead ? (uint32_t)tid : kbody + (uint32_t)tid;
-      skb[ko + e] = kin[g0 + e];
-    }
-    if (VB && (uint32_t)tid >= 64 && (uint32_t)tid < 64 + tn - vbody) {
-      const uint32_t t2 = tid - 64;
-      const uint32_t e = t2 < vhead ? t2 : vbody + t2;
-      svb[vo + e] = vin[g0 + e];
-    }
-    // hist-block offsets of this tile's buckets (needed much later)
-    uint32_t boff[TL::NBC / NT];
-#pragma unroll
-    for (int r = 0; r < TL::NBC / NT; ++r) {
-      const uint32_t b = tid + r * NT;
-      boff[r] = b < nb ? (uint32_t)(scan[P.cnt_base + (uint64_t)b * P.nrows + G.row] - P.scanbase)
-                       : 0u;
+    // hist-block offsets of this thread's bucket pair (needed much later)
+    // (raw u64 values: nothing waits on these loads before the look-back)
+    uint64_t bo0 = 0, bo1 = 0;
+    if ((uint32_t)tid < npair) {
+      const uint64_t* col = scan + P.cnt_base + G.row;
+      const uint64_t nr = P.nrows;
+      bo0 = col[(uint64_t)(2 * tid) * nr];
+      if ((uint32_t)(2 * tid + 1) < nb) bo1 = col[(uint64_t)(2 * tid + 1) * nr];
     }
     if (G.seg != s_seg) {  // block-uniform
       load_tables<K>(P, heavy_pool, hz_pool, split_idx, hk, si, hz);
     }
-    // next tile: geometry + plan into the other slot, data into L2
-    if (warp == 1 && t + gridDim.x < ntile) {
-      resolve(t + gridDim.x, cur ^ 1);
-      if (lane == 0) {
-        const TileGeo& N = sgeo[cur ^ 1];
-        uint32_t o2, h2, b2;
-        const uint32_t kb2 = tile_body<K>(N.g0, N.tn, o2, h2, b2);
-        if (kb2) prefetch_l2(kin + N.g0 + h2, kb2);
-        if (VB) {
-          const uint32_t vb2 = tile_body<V>(N.g0, N.tn, o2, h2, b2);
-          if (vb2) prefetch_l2(vin + N.g0 + h2, vb2);
-        }
-      }
-    }
     __syncthreads();
+    PH(1)
     if (tid == 0) s_seg = G.seg;
     mbar_wait(&bar[0], phase);
     phase ^= 1u;
+    PH(2)
     const K* sk = skb + ko;
     const V* sv = svb + vo;
+
     // ---- route + per-warp rank (lane-striped within the warp sub-tile) ----
     uint32_t bk[IPT], lr[IPT];
     auto rank_one = [&](int i, uint32_t b) {
@@ -230,24 +285,18 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
       bk[i] = b;
       lr[i] = (old >> sh) & 0xffffu;
     };
-    const bool full = tn == (uint32_t)T;
-    if (!SPLIT && !(P.flags & (PF_HEAVY | PF_OVF))) {
-      // plain digit: zone = (key >> shift) & mask (sampler.py:76-88 light ids)
+    if (!SPLIT && full && !(P.flags & PF_HEAVY)) {
+      // light digit, overflow bucket by select (sampler.py:76-100 bucket ids;
+      // without an overflow bucket the all-ones key maps to its own digit)
       const uint32_t shift = P.shift, mask = (1u << P.gamma) - 1u;
-      if (full) {
+      const bool ovf = (P.flags & PF_OVF) != 0;
+      const K thr = ovf ? P.ovf_thr : ~K(0);
+      const uint32_t ovfb = ovf ? nb - 1 : ((uint32_t)(~K(0) >> shift) & mask);
 #pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-          rank_one(i, (uint32_t)(sk[warp * WS + i * 32 + lane] >> shift) & mask);
-          __syncwarp();
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-          const uint32_t e = warp * WS + i * 32 + lane;
-          bk[i] = 0xFFFFu;
-          if (e < tn) rank_one(i, (uint32_t)(sk[e] >> shift) & mask);
-          __syncwarp();
-        }
+      for (int i = 0; i < IPT; ++i) {
+        const K key = sk[warp * WS + i * 32 + lane];
+        rank_one(i, key >= thr ? ovfb : ((uint32_t)(key >> shift) & mask));
+        __syncwarp();
       }
     } else {
       const Router<K> R = make_router<K>(P, hz, hk);
@@ -265,25 +314,47 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
       }
     }
     __syncthreads();
-    // ---- per bucket pair: prefix over warps, tile counts, publish ----
-    uint32_t* myst = status + (uint64_t)t * nbs;
-    for (uint32_t j = tid; j < (nb + 1) / 2; j += NT) {
-      uint32_t s = 0;
+    PH(3)
+
+    // ---- bucket pair j = tid: prefix over warps, tile counts (published
+    // for the later tiles of the block), exclusive scan over the tile ----
+    uint32_t s = 0;
+    if ((uint32_t)tid < npair) {
 #pragma unroll
       for (int w = 0; w < NW; ++w) {
-        const uint32_t x = wh[w * HW + j];
-        wh[w * HW + j] = s;
+        const uint32_t x = wh[w * HW + tid];
+        wh[w * HW + tid] = s;
         s += x;
       }
-      tst[2 * j] = s & 0xffffu;
-      tst[2 * j + 1] = s >> 16;
-      if (kt + 1 < LB) {  // only later tiles of the block read it
-        st_volatile(myst + 2 * j, ST_AGG | (s & 0xffffu));
-        if (2 * j + 1 < nb) st_volatile(myst + 2 * j + 1, ST_AGG | (s >> 16));
+      if (kt + 1 < LB) st_volatile(status + (uint64_t)t * nbs + tid, s | ST_VALID);
+    }
+    const uint32_t ptot = (s & 0xffffu) + (s >> 16);
+    uint32_t incl = ptot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_wt[warp] = incl;
+    __syncthreads();
+    PH(4)
+    {
+      uint32_t wp = lane < NW ? s_wt[lane] : 0u;
+#pragma unroll
+      for (int o = 1; o < NW; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, wp, o);
+        if (lane >= o) wp += y;
+      }
+      const uint32_t wex = __shfl_sync(FULL, wp, (warp + 31) & 31);
+      const uint32_t ex = (warp ? wex : 0u) + incl - ptot;
+      if ((uint32_t)tid < npair) {
+        tst[2 * tid] = ex;
+        tst[2 * tid + 1] = ex + (s & 0xffffu);
       }
     }
     __syncthreads();
-    block_exscan<NT>(tst, (int)nb, s_tmp);
+    PH(5)
+
     // ---- placement (regroup by bucket in SMEM) ----
     if (full) {
 #pragma unroll
@@ -305,53 +376,92 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
     // each warp read only its own counters above: reset them for the next tile
     __syncwarp();
     for (uint32_t i = lane; i < HW; i += 32) mywh[i] = 0u;
-    // ---- bucket bases: block offsets + earlier tiles of the block ----
-    {
-      const uint32_t* st0 = status + (uint64_t)(t - kt) * nbs;
-#pragma unroll
-      for (int r = 0; r < TL::NBC / NT; ++r) {
-        const uint32_t b = tid + r * NT;
-        if (b < nb) {
-          uint32_t v[LB - 1];
-#pragma unroll
-          for (int j = 0; j < LB - 1; ++j)
-            if ((uint32_t)j < kt) v[j] = ld_volatile(st0 + (uint64_t)j * nbs + b);
-          uint32_t excl = 0;
-#pragma unroll
-          for (int j = 0; j < LB - 1; ++j) {
-            if ((uint32_t)j < kt) {
-              while ((v[j] >> 30) == 0u) v[j] = ld_volatile(st0 + (uint64_t)j * nbs + b);
-              excl += v[j] & ST_VAL;
-            }
-          }
-          db[b] = boff[r] + excl - tst[b];
+    PH(6)
+    // next tile: geometry + plan into the other slot, data into L2
+    if (warp == 1 && t + gridDim.x < ntile) {
+      resolve(t + gridDim.x, cur ^ 1);
+      if (lane == 0) {
+        const TileGeo& N = sgeo[cur ^ 1];
+        uint32_t o2, h2, b2;
+        const uint32_t kb2 = tile_body<K>(N.g0, N.tn, o2, h2, b2);
+        if (kb2) prefetch_l2(kin + N.g0 + h2, kb2);
+        if (VB) {
+          const uint32_t vb2 = tile_body<V>(N.g0, N.tn, o2, h2, b2);
+          if (vb2) prefetch_l2(vin + N.g0 + h2, vb2);
         }
       }
     }
+
+    // ---- bucket bases of pair j: block offsets + earlier tiles of the
+    // block (look-back over <= LB-1 status words, read in parallel) ----
+    if ((uint32_t)tid < npair) {
+      const uint32_t* st0 = status + (uint64_t)(t - kt) * nbs + tid;
+      uint32_t v[LB - 1];
+#pragma unroll
+      for (int j = 0; j < LB - 1; ++j)
+        if ((uint32_t)j < kt) v[j] = ld_volatile(st0 + (uint64_t)j * nbs);
+      uint32_t ex = 0;
+#pragma unroll
+      for (int j = 0; j < LB - 1; ++j) {
+        if ((uint32_t)j < kt && !(DTS_SCATTER_EXP & 2)) {
+          while (!(v[j] & ST_VALID)) {
+            PH_SPIN
+            __nanosleep(64);
+            v[j] = ld_volatile(st0 + (uint64_t)j * nbs);
+          }
+          ex += v[j] & ST_MASK;
+        }
+      }
+      const uint32_t sb = (uint32_t)P.scanbase;
+      db[2 * tid] = (uint32_t)bo0 - sb + (ex & 0xffffu) - tst[2 * tid];
+      db[2 * tid + 1] = (uint32_t)bo1 - sb + (ex >> 16) - tst[2 * tid + 1];
+    }
+    PH(7)
     __syncthreads();
+    PH(8)
+
     // ---- write the bucket runs; the in-step order check (dts_rank.cuh) is
     // fused: pairs (p, p+1) of one group must ascend.  If a pair does not,
     // the groups are re-sorted and the tile is written again (same
     // addresses, corrected values). ----
-    K* ko_seg = kout + P.offset;
-    V* vo_seg = VB ? vout + P.offset : nullptr;
+    // segment base pointers kept opaque so each store address is one
+    // IMAD.WIDE.U32 of the u32 position (no 64-bit re-association); st_global
+    // keeps the stores in the global space
+    K* ko_seg = opaque_ptr(kout + P.offset);
+    V* vo_seg = VB ? opaque_ptr(vout + P.offset) : nullptr;
     bool bad = false;
+    if (full) {
 #pragma unroll
-    for (int it = 0; it < IPT; ++it) {
-      const uint32_t p = it * NT + tid;
-      const uint32_t wd = (full || p < tn) ? pk[p] : 0xFFFFFFFFu;
-      uint32_t nx = __shfl_down_sync(FULL, wd, 1);
-      if (lane == 31) nx = p + 1 < tn ? pk[p + 1] : 0xFFFFFFFFu;
-      bad |= ((wd ^ nx) < 32u) && (nx < wd);
-      if (full || p < tn) {
-        const uint32_t bb = wd >> 16, e = wd & 0xffffu;
-        const uint32_t d = db[bb] + p;
-        ko_seg[d] = sk[e];
-        if (VB) vo_seg[d] = sv[e];
+      for (int it = 0; it < IPT; ++it) {
+        const uint32_t p = it * NT + tid;
+        const uint32_t wd = pk[p], nx = pk[p + 1];
+        bad |= ((wd ^ nx) < 32u) & (nx < wd);
+        const uint32_t e = wd & 0xffffu;
+        const uint32_t d = db[wd >> 16] + p;
+        if (DTS_SCATTER_EXP & 1) {
+          bad |= ((uint32_t)sk[e] ^ (uint32_t)sv[e] ^ d) == 0x12345u;
+        } else {
+          st_global(ko_seg + d, sk[e]);
+          if (VB) st_global(vo_seg + d, sv[e]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int it = 0; it < IPT; ++it) {
+        const uint32_t p = it * NT + tid;
+        if (p < tn) {
+          const uint32_t wd = pk[p], nx = pk[p + 1];
+          bad |= ((wd ^ nx) < 32u) & (nx < wd);
+          const uint32_t e = wd & 0xffffu;
+          const uint32_t d = db[wd >> 16] + p;
+          st_global(ko_seg + d, sk[e]);
+          if (VB) st_global(vo_seg + d, sv[e]);
+        }
       }
     }
     if (__any_sync(FULL, bad) && lane == 0) s_fix = 1u;
     __syncthreads();
+    PH(9)
     if (s_fix || DTS_FORCE_FIXUP) {
       for (uint32_t p = tid; p < tn; p += NT) {
         const uint32_t x = pk[p];
@@ -374,6 +484,7 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
       if (tid == 0) s_fix = 0u;
     }
   }
+  PH_DONE
 }
 
 }  // namespace dts

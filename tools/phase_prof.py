@@ -1,0 +1,30 @@
+"""k_scatter phase profile (needs libdts_phase.so: make -C csrc ../_lib/libdts_phase.so).
+DTS_LIB=paper_2401_00710_b200/_lib/libdts_phase.so python tools/phase_prof.py [n]"""
+import ctypes, sys
+import torch
+sys.path.insert(0, ".")
+from paper_2401_00710_b200 import SortConfig, _lib
+from paper_2401_00710_b200.dtsort import sort_device
+
+n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 10**9
+L = _lib.lib()
+L.dts_debug_phases.restype = ctypes.c_int
+buf = (ctypes.c_ulonglong * 16)()
+g = torch.Generator(device="cuda"); g.manual_seed(0)
+src = torch.randint(0, 10**9, (n,), generator=g, device="cuda", dtype=torch.int64).to(torch.int32)
+k = torch.empty_like(src); v = torch.empty_like(src)
+names = ["top->issue", "issue->bar1", "tma wait", "rank", "prefix+scan", "tst", "placement",
+         "lookback", "bar(lookback)", "write-out"]
+for rep in range(2):
+    k.copy_(src); torch.arange(n, out=v); torch.cuda.synchronize()
+    L.dts_debug_phases(buf, 16, 1)
+    r = sort_device(k, v, SortConfig(), 0, report=True)
+    torch.cuda.synchronize()
+    L.dts_debug_phases(buf, 16, 0)
+tiles = r.kernel_records["scatter"] / 4608.0
+ctas = buf[14]
+tot = sum(buf[i] for i in range(10))
+print(f"tiles ~{tiles:.0f}  CTA-runs {ctas}  spins {buf[15]}")
+for i, nm in enumerate(names):
+    print(f"{nm:16s} {buf[i]/tiles:9.0f} cycles/tile  {100*buf[i]/tot:5.1f}%")
+print(f"{'total':16s} {tot/tiles:9.0f} cycles/tile")
