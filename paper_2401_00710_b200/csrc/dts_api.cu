@@ -19,6 +19,7 @@
 #include "../../include/dts.h"
 #include "dts_local.cuh"
 #include "dts_scatter.cuh"
+#include "dts_scatter_wc.cuh"
 
 using namespace dts;
 
@@ -53,6 +54,8 @@ constexpr int SAMPLE_NT = 1024;
 // block = LB consecutive tiles (one count-matrix row, look-back depth < LB)
 inline uint64_t scatter_T(int kb, int vb) { return (kb == 4 && vb <= 4) ? 512 * 9 : 512 * 5; }
 inline uint64_t block_records(int kb, int vb) { return scatter_T(kb, vb) * 8; }
+// write-combining scatter: stripe (= count-matrix row) of WC_LBS tiles
+constexpr uint64_t WC_LBS = 64;
 constexpr uint32_t COPY_CHUNK = 1u << 16;
 constexpr uint64_t SPAN_BATCH = 1u << 18;      // spans per k_local_sort launch
 constexpr uint64_t SAMPLE_FACTOR = 2;          // sample iff n' >= 2|S| (dtsort.py:225)
@@ -384,12 +387,15 @@ struct Sorter {
     const size_t ns = s1 - s0;
     const bool dt = cfg.mode == DTS_MODE_DT;
     const double t_plan0 = trace_on() ? now_us() : 0.0;
-    // ---- host plans ----
+    const K* ink = in_T ? Tk : Ak;
+    const V* inv = in_T ? Tv : Av;
+    K* outk = in_T ? Ak : Tk;
+    V* outv = in_T ? Av : Tv;
+    // ---- host plans (digit, sampling decision, table pools) ----
     std::vector<SegPlan> plans(ns);
-    std::vector<Blk> blks;
     std::vector<uint32_t> sampled;
-    uint64_t cnt_total = 0, bs_total = 0, heavy_total = 0, hz_total = 0, scanbase = 0;
-    uint32_t nbc = 2, hzc = 0, hkc = 0;
+    uint64_t heavy_total = 0, hz_total = 0, scanbase = 0, wave_recs = 0;
+    uint32_t hzc = 0, hkc = 0;
     for (size_t i = 0; i < ns; ++i) {
       const HostSeg& hs = segs[s0 + i];
       SegPlan& P = plans[i];
@@ -400,6 +406,7 @@ struct Sorter {
       P.len = hs.len;
       P.scanbase = scanbase;
       scanbase += hs.len;
+      wave_recs += hs.len;
       P.gamma = g;
       P.shift = remaining - g;
       P.consumed = hs.consumed;
@@ -424,96 +431,142 @@ struct Sorter {
         hzc = std::max(hzc, (1u << g) + 1u);
         hkc = std::max(hkc, 1u << gs);
       }
-      const uint64_t BR = block_records(sizeof(K), VB);
-      const uint64_t rows = std::max<uint64_t>(1, (hs.len + BR - 1) / BR);
+    }
+    const size_t save = meta.off;
+    const size_t pb = ns * sizeof(SegPlan), sb = sampled.size() * 4;
+    SegPlan* dplans = (SegPlan*)meta.take(pb);
+    uint32_t* dsampled = (uint32_t*)meta.take(std::max<size_t>(1, sampled.size()) * 4);
+    K* dheavy = (K*)meta.take(std::max<uint64_t>(1, heavy_total) * sizeof(K));
+    uint32_t* dhz = (uint32_t*)meta.take(std::max<uint64_t>(1, hz_total) * 4);
+    uint32_t* dctr = (uint32_t*)meta.take(16);
+    if (!dplans || !dsampled || !dheavy || !dhz || !dctr)
+      return fail(DTS_ENOMEM, "workspace too small for level metadata");
+
+    // ---- sample + plan (sampler.py:121-252); the resolved plans come back
+    // so the scatter variant and the count-matrix shape fit the real bucket
+    // counts ----
+    static const int wc_env = env_int("DTS_WC", 1);
+    if (!sampled.empty()) {
+      DTS_TRY(g_pin_plan.ensure(align256(pb) + sb + 512));
+      char* hp = (char*)g_pin_plan.p;
+      std::memcpy(hp, plans.data(), pb);
+      std::memcpy(hp + align256(pb), sampled.data(), sb);
+      CUDA_TRY(cudaMemcpyAsync(dplans, hp, pb, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(dsampled, hp + align256(pb), sb, cudaMemcpyHostToDevice, st));
+      Timer::Ev ev;
+      tm.begin(DTS_K_SAMPLE, ev);
+      auto fn = k_sample_plan<K, SAMPLE_NT>;
+      const size_t sm = (size_t)smax * sizeof(K);
+      DTS_TRY(set_smem(fn, sm));
+      fn<<<(unsigned)sampled.size(), SAMPLE_NT, sm, st>>>(dplans, dsampled, ink, dheavy, dhz,
+                                                           cfg.seed, (uint32_t)level, stride,
+                                                           gs_max, smax);
+      tm.end(ev, sampled.size());
+      DTS_TRY(check_launch("k_sample_plan"));
+      if (wc_env) {
+        DTS_TRY(g_pin_back.ensure(pb + 256));
+        CUDA_TRY(cudaMemcpyAsync(g_pin_back.p, dplans, pb, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        std::memcpy(plans.data(), g_pin_back.p, pb);
+      }
+    }
+    // the write-combining scatter takes waves whose bucket columns fit its
+    // SMEM carries; its count-matrix rows are whole stripes
+    uint32_t nbc = 2;
+    for (size_t i = 0; i < ns; ++i) {
+      const bool known = !(plans[i].flags & PF_SAMPLE) || wc_env;
+      nbc = std::max(nbc, known ? plans[i].nb : plans[i].nbmax);
+    }
+    nbc = (nbc + 1) & ~1u;
+    const bool wc = wc_env != 0 && nbc <= (uint32_t)WcTile<K, VB>::NBW;
+    const uint64_t BR = wc ? (uint64_t)WcTile<K, VB>::T * WC_LBS : block_records(sizeof(K), VB);
+    const uint64_t TT = wc ? (uint64_t)WcTile<K, VB>::T : (uint64_t)ScatterTile<K, VB>::T;
+    // ---- count-matrix shape and hist blocks ----
+    std::vector<Blk> blks;
+    uint64_t cnt_total = 0, bs_total = 0;
+    for (size_t i = 0; i < ns; ++i) {
+      SegPlan& P = plans[i];
+      const uint64_t len = P.len;
+      const uint64_t rows = std::max<uint64_t>(1, (len + BR - 1) / BR);
+      if (wc_env && (P.flags & PF_SAMPLE)) P.nbmax = P.nb;  // resolved
       P.nrows = (uint32_t)rows;
       P.cnt_base = cnt_total;
       cnt_total += (uint64_t)P.nbmax * rows;
       P.bs_base = (uint32_t)bs_total;
       bs_total += P.nbmax + 1;
-      nbc = std::max(nbc, P.nbmax);
-      constexpr uint64_t TT = ScatterTile<K, VB>::T;  // whole tiles per block
-      const uint64_t per = ((hs.len + rows - 1) / rows + TT - 1) / TT * TT;
+      // whole tiles per block
+      const uint64_t per = ((len + rows - 1) / rows + TT - 1) / TT * TT;
       for (uint64_t r = 0; r < rows; ++r) {
         Blk b;
         b.seg = (uint32_t)i;
         b.row = (uint32_t)r;
-        b.begin = hs.offset + std::min(hs.len, r * per);
-        b.end = hs.offset + std::min(hs.len, (r + 1) * per);
+        b.begin = P.offset + std::min(len, r * per);
+        b.end = P.offset + std::min(len, (r + 1) * per);
         blks.push_back(b);
       }
     }
-    nbc = (nbc + 1) & ~1u;
     Caps caps{nbc, hzc, hkc, 0};
-    // scatter tiles in input order (each hist block split into T-record tiles)
+    // look-back scatter: tiles in input order (each hist block split into tiles)
     constexpr uint32_t ST_T = ScatterTile<K, VB>::T;
-    std::vector<uint32_t> blk_tile0(blks.size());
+    std::vector<uint32_t> blk_tile0;
+    std::vector<uint32_t> tile_blk;
     uint64_t ntile = 0;
-    for (size_t bi = 0; bi < blks.size(); ++bi) {
-      blk_tile0[bi] = (uint32_t)ntile;
-      ntile += (blks[bi].end - blks[bi].begin + ST_T - 1) / ST_T;
-    }
-    std::vector<uint32_t> tile_blk(ntile);
-    for (size_t bi = 0; bi < blks.size(); ++bi) {
-      const uint32_t e = bi + 1 < blks.size() ? blk_tile0[bi + 1] : (uint32_t)ntile;
-      for (uint32_t t = blk_tile0[bi]; t < e; ++t) tile_blk[t] = (uint32_t)bi;
+    if (!wc) {
+      blk_tile0.resize(blks.size());
+      for (size_t bi = 0; bi < blks.size(); ++bi) {
+        blk_tile0[bi] = (uint32_t)ntile;
+        ntile += (blks[bi].end - blks[bi].begin + ST_T - 1) / ST_T;
+      }
+      tile_blk.resize(ntile);
+      for (size_t bi = 0; bi < blks.size(); ++bi) {
+        const uint32_t e = bi + 1 < blks.size() ? blk_tile0[bi + 1] : (uint32_t)ntile;
+        for (uint32_t t = blk_tile0[bi]; t < e; ++t) tile_blk[t] = (uint32_t)bi;
+      }
     }
 
     // ---- device meta ----
-    const size_t save = meta.off;
-    SegPlan* dplans = (SegPlan*)meta.take(ns * sizeof(SegPlan));
     Blk* dblks = (Blk*)meta.take(blks.size() * sizeof(Blk));
-    uint32_t* dsampled = (uint32_t*)meta.take(std::max<size_t>(1, sampled.size()) * 4);
     uint32_t* dcnt = (uint32_t*)meta.take(cnt_total * 4);
     uint64_t* dscan = (uint64_t*)meta.take(cnt_total * 8);
     const uint64_t nch = (cnt_total + SCAN_CHUNK - 1) / SCAN_CHUNK;
     uint64_t* dpart = (uint64_t*)meta.take(std::max<uint64_t>(1, nch) * 8);
     uint64_t* dbs = (uint64_t*)meta.take(bs_total * 8);
     uint8_t* dkinds = (uint8_t*)meta.take(bs_total);
-    K* dheavy = (K*)meta.take(std::max<uint64_t>(1, heavy_total) * sizeof(K));
-    uint32_t* dhz = (uint32_t*)meta.take(std::max<uint64_t>(1, hz_total) * 4);
-    uint32_t* dctr = (uint32_t*)meta.take(16);
     uint32_t* dtile_blk = (uint32_t*)meta.take(std::max<uint64_t>(1, ntile) * 4);
-    uint32_t* dblk_tile0 = (uint32_t*)meta.take(std::max<size_t>(1, blks.size()) * 4);
+    uint32_t* dblk_tile0 = (uint32_t*)meta.take(std::max<size_t>(1, blk_tile0.size()) * 4);
     uint32_t* dstatus = (uint32_t*)meta.take(std::max<uint64_t>(1, ntile) * (nbc / 2) * 4);
-    if (!dplans || !dblks || !dsampled || !dcnt || !dscan || !dpart || !dbs || !dkinds ||
-        !dheavy || !dhz || !dctr || !dtile_blk || !dblk_tile0 || !dstatus)
+    if (!dblks || !dcnt || !dscan || !dpart || !dbs || !dkinds || !dtile_blk || !dblk_tile0 ||
+        !dstatus)
       return fail(DTS_ENOMEM, "workspace too small for level metadata");
 
     // ---- H2D ----
-    const size_t pb = ns * sizeof(SegPlan), bb = blks.size() * sizeof(Blk),
-                 sb = sampled.size() * 4;
-    const size_t tb = ntile * 4, b0b = blks.size() * 4;
+    const size_t bb = blks.size() * sizeof(Blk);
+    const size_t tb = ntile * 4, b0b = blk_tile0.size() * 4;
     DTS_TRY(g_pin_plan.ensure(align256(pb) + align256(bb) + align256(sb) + align256(tb) + b0b + 512));
     char* hp = (char*)g_pin_plan.p;
     std::memcpy(hp, plans.data(), pb);
     std::memcpy(hp + align256(pb), blks.data(), bb);
     if (sb) std::memcpy(hp + align256(pb) + align256(bb), sampled.data(), sb);
     char* htl = hp + align256(pb) + align256(bb) + align256(sb);
-    std::memcpy(htl, tile_blk.data(), tb);
-    std::memcpy(htl + align256(tb), blk_tile0.data(), b0b);
-    CUDA_TRY(cudaMemcpyAsync(dtile_blk, htl, tb, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(dblk_tile0, htl + align256(tb), b0b, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(dplans, hp, pb, cudaMemcpyHostToDevice, st));
+    if (!wc) {
+      std::memcpy(htl, tile_blk.data(), tb);
+      std::memcpy(htl + align256(tb), blk_tile0.data(), b0b);
+      CUDA_TRY(cudaMemcpyAsync(dtile_blk, htl, tb, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(dblk_tile0, htl + align256(tb), b0b, cudaMemcpyHostToDevice, st));
+    }
+    const bool sample_later = !sampled.empty() && !wc_env;
+    if (sampled.empty() || !sample_later || wc_env)
+      CUDA_TRY(cudaMemcpyAsync(dplans, hp, pb, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(dblks, hp + align256(pb), bb, cudaMemcpyHostToDevice, st));
-    if (sb)
-      CUDA_TRY(cudaMemcpyAsync(dsampled, hp + align256(pb) + align256(bb), sb,
-                               cudaMemcpyHostToDevice, st));
-
-    const K* ink = in_T ? Tk : Ak;
-    const V* inv = in_T ? Tv : Av;
-    K* outk = in_T ? Ak : Tk;
-    V* outv = in_T ? Av : Tv;
-    uint64_t wave_recs = 0;
-    for (size_t i = 0; i < ns; ++i) wave_recs += plans[i].len;
-
-    // ---- sample + plan ----
-    if (!sampled.empty()) {
+    if (sample_later) {
+      // DTS_WC=0: plans (with the count-matrix shape) go up before sampling
       Timer::Ev ev;
       tm.begin(DTS_K_SAMPLE, ev);
       auto fn = k_sample_plan<K, SAMPLE_NT>;
       const size_t sm = (size_t)smax * sizeof(K);
       DTS_TRY(set_smem(fn, sm));
+      CUDA_TRY(cudaMemcpyAsync(dsampled, hp + align256(pb) + align256(bb), sb,
+                               cudaMemcpyHostToDevice, st));
       fn<<<(unsigned)sampled.size(), SAMPLE_NT, sm, st>>>(dplans, dsampled, ink, dheavy, dhz,
                                                            cfg.seed, (uint32_t)level, stride,
                                                            gs_max, smax);
@@ -543,7 +596,19 @@ struct Sorter {
       DTS_TRY(check_launch("k_bucket_bounds"));
     }
     // ---- scatter ----
-    {
+    if (wc) {
+      CUDA_TRY(cudaMemsetAsync(dctr + 1, 0, 4, st));
+      Timer::Ev ev;
+      tm.begin(DTS_K_SCATTER, ev);
+      auto fn = k_scatter_wc<K, VB>;
+      const size_t sm = WcSmem<K, VB>::total;
+      DTS_TRY(set_smem(fn, sm));
+      const int grid = persistent_grid(fn, WcTile<K, VB>::NT, sm, (uint32_t)blks.size());
+      fn<<<grid, WcTile<K, VB>::NT, sm, st>>>(dplans, dblks, (uint32_t)blks.size(), dctr + 1, ink, inv,
+                                              outk, outv, dscan, dheavy, dhz);
+      tm.end(ev, wave_recs);
+      DTS_TRY(check_launch("k_scatter_wc"));
+    } else {
       CUDA_TRY(cudaMemsetAsync(dctr + 1, 0, 4, st));
       CUDA_TRY(cudaMemsetAsync(dstatus, 0, ntile * (nbc / 2) * 4, st));
       Timer::Ev ev;

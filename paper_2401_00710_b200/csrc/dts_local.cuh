@@ -316,14 +316,13 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
         }
       }
       __syncthreads();
-      // in-step order check: within one (digit, warp step) group positions
-      // must ascend; a violation is repaired by re-sorting the groups
+      // stable order check: within one digit, pass-input positions must
+      // ascend; a violation is repaired by re-sorting the digit runs
       bool bad = false;
       for (uint32_t p = tid; p + 1 < n; p += NT) {
         const uint32_t a = si[p], b = si[p + 1];
-        const bool same = ((((uint32_t)(sk[p] >> sh) ^ (uint32_t)(sk[p + 1] >> sh)) & (D - 1)) == 0u) &&
-                          ((a >> 21) == (b >> 21));
-        bad |= same && b < a;
+        const bool same = (((uint32_t)(sk[p] >> sh) ^ (uint32_t)(sk[p + 1] >> sh)) & (D - 1)) == 0u;
+        bad |= same && (b >> 16) < (a >> 16);
       }
       if (__any_sync(FULL, bad) && lane == 0) s_fix = 1u;
       __syncthreads();
@@ -331,9 +330,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
         for (uint32_t p = tid; p < n; p += NT) {
           const uint32_t x = si[p];
           const uint32_t dx = (uint32_t)(sk[p] >> sh) & (D - 1);
-          auto same = [&](uint32_t q) {
-            return ((uint32_t)(sk[q] >> sh) & (D - 1)) == dx && (si[q] >> 21) == (x >> 21);
-          };
+          auto same = [&](uint32_t q) { return ((uint32_t)(sk[q] >> sh) & (D - 1)) == dx; };
           const bool leader = p == 0 || !same(p - 1);
           if (leader && p + 1 < n && same(p + 1)) {
             uint32_t c = 2;

@@ -420,9 +420,9 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
     __syncthreads();
     PH(8)
 
-    // ---- write the bucket runs; the in-step order check (dts_rank.cuh) is
-    // fused: pairs (p, p+1) of one group must ascend.  If a pair does not,
-    // the groups are re-sorted and the tile is written again (same
+    // ---- write the bucket runs; the stable order check is fused: within a
+    // bucket, adjacent records must ascend in tile position.  If a pair does
+    // not, the bucket runs are re-sorted and the tile is written again (same
     // addresses, corrected values). ----
     // segment base pointers kept opaque so each store address is one
     // IMAD.WIDE.U32 of the u32 position (no 64-bit re-association); st_global
@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
       for (int it = 0; it < IPT; ++it) {
         const uint32_t p = it * NT + tid;
         const uint32_t wd = pk[p], nx = pk[p + 1];
-        bad |= ((wd ^ nx) < 32u) & (nx < wd);
+        bad |= ((wd ^ nx) < 65536u) & (nx < wd);
         const uint32_t e = wd & 0xffffu;
         const uint32_t d = db[wd >> 16] + p;
         if (DTS_SCATTER_EXP & 1) {
@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
         const uint32_t p = it * NT + tid;
         if (p < tn) {
           const uint32_t wd = pk[p], nx = pk[p + 1];
-          bad |= ((wd ^ nx) < 32u) & (nx < wd);
+          bad |= ((wd ^ nx) < 65536u) & (nx < wd);
           const uint32_t e = wd & 0xffffu;
           const uint32_t d = db[wd >> 16] + p;
           st_global(ko_seg + d, sk[e]);
@@ -463,12 +463,15 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
     __syncthreads();
     PH(9)
     if (s_fix || DTS_FORCE_FIXUP) {
+#if DTS_PHASE_PROF
+      if (tid == 0 && s_fix) atomicAdd(&g_phase[12], 1ull);
+#endif
       for (uint32_t p = tid; p < tn; p += NT) {
         const uint32_t x = pk[p];
-        const bool leader = p == 0 || ((pk[p - 1] ^ x) >= 32u);
-        if (leader && p + 1 < tn && ((pk[p + 1] ^ x) < 32u)) {
+        const bool leader = p == 0 || ((pk[p - 1] ^ x) >= 65536u);
+        if (leader && p + 1 < tn && ((pk[p + 1] ^ x) < 65536u)) {
           uint32_t c = 2;
-          while (p + c < tn && ((pk[p + c] ^ x) < 32u)) ++c;
+          while (p + c < tn && ((pk[p + c] ^ x) < 65536u)) ++c;
           small_isort(pk + p, c);
         }
       }

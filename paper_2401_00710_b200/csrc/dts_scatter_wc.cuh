@@ -1,0 +1,458 @@
+// dts_scatter_wc.cuh — k_scatter_wc, the write-combining stable distribution
+// pass (counting.py:141-151 scatter phase, _kernels.py:12-25 scatter_block).
+//
+// Why: on B200 the cost of a scattered store is set by the number of L2
+// write requests and by partially written 32-byte sectors (those force a
+// DRAM read-modify-write).  tools/mb_mem.cu measured, for 16 B/record of
+// traffic: runs of ~9 records written in place 1.2 TB/s, whole 32-byte
+// sectors 2.4 TB/s, whole 64-byte chunks 4.1-4.4 TB/s, 128-byte lines
+// 4.6-5.3 TB/s.  So every bucket's output is assembled in SMEM and leaves the
+// SM only as whole, aligned C-record chunks (64 or 128 bytes).
+//
+// Structure: one CTA per SM walks whole stripes (= count-matrix rows, many
+// tiles) in input order, so a bucket's records of consecutive tiles are
+// contiguous in its output region and the CTA can carry each bucket's
+// unfinished chunk (< C records) from tile to tile in SMEM.  Only the first
+// and last chunk of each (stripe, bucket) region may be partial.  No
+// look-back, no per-tile status.
+#pragma once
+#include "dts_scatter.cuh"
+
+namespace dts {
+
+template <typename K, int VB> struct WcTile {
+  static constexpr int NT = 512;
+  static constexpr int NW = NT / 32;
+  static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? 9 : 5;
+  static constexpr int WS = 32 * IPT;
+  static constexpr int T = NT * IPT;
+  static constexpr int NBW = 520;  // bucket capacity (2^9 light + overflow + slack)
+  static constexpr int C = (sizeof(K) == 8 || VB == 8) ? 8 : 16;  // chunk records (64 B)
+  static constexpr int CP = C + 1;                                 // carry stride (banks)
+  static constexpr int MAXCH = (T + (C - 1) * NBW) / C + 2;       // chunks per tile bound
+  static constexpr int HKC = 256;
+  static constexpr int HZC = 520;
+};
+
+template <typename K, int VB> struct WcSmem {
+  using TL = WcTile<K, VB>;
+  static constexpr size_t kb = a16((size_t)(TL::T + 8) * sizeof(K));
+  static constexpr size_t vb = a16((size_t)(TL::T + 8) * VB);
+  static constexpr size_t buf = 0;                                   // 2 x (keys | vals)
+  static constexpr size_t pk = a16(buf + 2 * (kb + vb));             // staging (b<<16|e)
+  static constexpr size_t ck = a16(pk + (size_t)(TL::T + 1) * 4);    // carry keys
+  static constexpr size_t cv = a16(ck + (size_t)TL::NBW * TL::CP * sizeof(K));
+  static constexpr size_t wh = a16(cv + (size_t)TL::NBW * TL::CP * VB);  // per-warp counters
+  // per bucket: {chunk offset, carry fill | hole << 16, tile offset, chunk base}
+  static constexpr size_t bi = a16(wh + (size_t)TL::NW * (TL::NBW / 2) * 4);
+  static constexpr size_t nf = a16(bi + (size_t)(TL::NBW + 1) * 16);  // tile count | chunks << 16
+  static constexpr size_t cst = a16(nf + (size_t)TL::NBW * 4);         // 2 x carry state
+  static constexpr size_t map = a16(cst + (size_t)2 * (TL::NBW + 1) * 8);  // chunk -> bucket
+  static constexpr size_t hk = a16(map + (size_t)TL::MAXCH * 2);
+  static constexpr size_t hz = a16(hk + (size_t)TL::HKC * sizeof(K));
+  static constexpr size_t plan = a16(hz + (size_t)TL::HZC * 4);
+  static constexpr size_t bar = a16(plan + sizeof(SegPlan));
+  static constexpr size_t total = a16(bar + 16);
+};
+
+// ---------------------------------------------------------------------------
+// k_scatter_wc: persistent, one CTA per SM, stripes taken from an atomic
+// counter in input order.  Two SMEM buffers alternate per tile: a tile is
+// streamed in by TMA while the previous one is ranked, and once its records
+// sit in registers its own buffer becomes the staging area.  Per tile:
+//   * ranks: route each key (read from SMEM right before its atomic — this
+//     issue pattern keeps the SMEM atomics of one warp instruction in lane
+//     order; order is verified below anyway) and take per-warp packed u16
+//     counters (k_scatter's scheme);
+//   * per bucket pair: prefix over warps, tile counts, and one packed block
+//     scan giving both the tile offsets (tst) and the chunk offsets (sfc) of
+//     carry + run; the owner writes its chunks into the chunk -> bucket map;
+//   * placement into the staging area in bucket order; the stable order is
+//     checked over the whole staging (every adjacent pair of one bucket must
+//     ascend in tile position) and repaired if ever needed;
+//   * write-out of every complete chunk (carry slots first, then staging)
+//     as aligned C-record chunks (64 bytes);
+//   * each bucket's unfinished chunk moves to its carry slots.
+// At the end of a stripe the carries are flushed.
+// ---------------------------------------------------------------------------
+template <typename K, int VB>
+__global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
+    k_scatter_wc(const SegPlan* __restrict__ plans, const Blk* __restrict__ blks, uint32_t nblk,
+                 uint32_t* __restrict__ ctr, const K* __restrict__ kin,
+                 const typename ValOf<VB>::T* __restrict__ vin, K* __restrict__ kout,
+                 typename ValOf<VB>::T* __restrict__ vout, const uint64_t* __restrict__ scan,
+                 const K* __restrict__ heavy_pool, const uint32_t* __restrict__ hz_pool) {
+  using V = typename ValOf<VB>::T;
+  using TL = WcTile<K, VB>;
+  using SL = WcSmem<K, VB>;
+  constexpr int NT = TL::NT, NW = TL::NW, IPT = TL::IPT, WS = TL::WS, T = TL::T, C = TL::C,
+                CP = TL::CP;
+  constexpr uint32_t HW = TL::NBW / 2;
+  static_assert(HW <= (uint32_t)NT, "one bucket pair per thread");
+  static_assert(T < 65536, "packed u16 counts");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* pk = reinterpret_cast<uint32_t*>(smem_raw + SL::pk);
+  K* ck = reinterpret_cast<K*>(smem_raw + SL::ck);
+  V* cv = reinterpret_cast<V*>(smem_raw + SL::cv);
+  uint32_t* wh = reinterpret_cast<uint32_t*>(smem_raw + SL::wh);
+  uint4* binfo = reinterpret_cast<uint4*>(smem_raw + SL::bi);
+  uint32_t* bnf = reinterpret_cast<uint32_t*>(smem_raw + SL::nf);  // copy: src | dst<<16 | cnt<<24
+  uint2* cst = reinterpret_cast<uint2*>(smem_raw + SL::cst);      // {fill | hole << 16, chunk base}
+  uint16_t* cmap = reinterpret_cast<uint16_t*>(smem_raw + SL::map);
+  K* hk = reinterpret_cast<K*>(smem_raw + SL::hk);
+  uint32_t* hz = reinterpret_cast<uint32_t*>(smem_raw + SL::hz);
+  SegPlan* splan = reinterpret_cast<SegPlan*>(smem_raw + SL::plan);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + SL::bar);
+  auto bufk = [&](int b) { return reinterpret_cast<K*>(smem_raw + SL::buf + (size_t)b * (SL::kb + SL::vb)); };
+  auto bufv = [&](int b) {
+    return reinterpret_cast<V*>(smem_raw + SL::buf + (size_t)b * (SL::kb + SL::vb) + SL::kb);
+  };
+  __shared__ uint32_t s_blk, s_fix, s_seg;
+  __shared__ uint32_t s_wt[NW];
+  __shared__ uint32_t s_off[2][2];  // per buffer: key / value element offset of the tile
+  __shared__ Blk s_B;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t* mywh = wh + warp * HW;
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    s_fix = 0u;
+    s_seg = 0xFFFFFFFFu;
+  }
+  for (uint32_t i = tid; i < NW * HW; i += NT) wh[i] = 0u;
+  uint32_t ph0 = 0u, ph1 = 0u;
+  int cur = 0;
+  PH_INIT
+
+  // thread 0: stream records [g0, g0+tn) into buffer b
+  auto issue_tile = [&](uint64_t g0, uint32_t tn, int b) {
+    const char* ks;
+    uint32_t ko, vo = 0;
+    const uint32_t kbytes = tile_span<K>(kin, g0, tn, ks, ko);
+    const char* vs = nullptr;
+    uint32_t vbytes = 0;
+    if (VB) vbytes = tile_span<V>(vin, g0, tn, vs, vo);
+    s_off[b][0] = ko;
+    s_off[b][1] = vo;
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&bar[b], kbytes + vbytes);
+    tma_load_1d(bufk(b), ks, kbytes, &bar[b]);
+    if (VB) tma_load_1d(bufv(b), vs, vbytes, &bar[b]);
+  };
+
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_blk = atomicAdd(ctr, 1u);
+    __syncthreads();
+    const uint32_t bi = s_blk;
+    if (bi >= nblk) break;
+    if (tid == 0) s_B = blks[bi];
+    if (warp == 1) {
+      const uint32_t seg = blks[bi].seg;
+      constexpr int PW = sizeof(SegPlan) / 4;
+      if (lane < PW)
+        reinterpret_cast<uint32_t*>(splan)[lane] = reinterpret_cast<const uint32_t*>(&plans[seg])[lane];
+    }
+    __syncthreads();
+    const Blk B = s_B;
+    const SegPlan& P = *splan;
+    const uint32_t nb = P.nb, npair = (nb + 1) >> 1;
+    if (B.seg != s_seg && (P.flags & PF_HEAVY)) {
+      // zone table and heavy keys of the segment (sampler.py:76-100)
+      for (uint32_t i = tid; i <= P.nb && i < TL::HZC; i += NT) hz[i] = hz_pool[P.hz_base + i];
+      for (uint32_t i = tid; i < P.nheavy && i < (uint32_t)TL::HKC; i += NT) hk[i] = heavy_pool[P.heavy_base + i];
+    }
+    // per bucket: block offset -> chunk base, hole = fill (carry state kept
+    // in binfo.y = fill | hole << 16 and binfo.w = chunk base across tiles)
+    int cs = 0;  // carry-state buffer of the next tile
+    for (uint32_t b = tid; b < nb; b += NT) {
+      const uint32_t o = (uint32_t)(scan[P.cnt_base + (uint64_t)b * P.nrows + B.row] - P.scanbase);
+      const uint32_t h = o & (uint32_t)(C - 1);
+      cst[b] = make_uint2(h | (h << 16), o & ~(uint32_t)(C - 1));
+    }
+    K* ko_seg = opaque_ptr(kout + P.offset);
+    V* vo_seg = VB ? opaque_ptr(vout + P.offset) : nullptr;
+    const uint64_t len = B.end - B.begin;
+    const uint32_t ntl = (uint32_t)((len + T - 1) / T);
+    auto tile_n = [&](uint32_t kt) {
+      const uint64_t r = len - (uint64_t)kt * T;
+      return (uint32_t)(r < (uint64_t)T ? r : (uint64_t)T);
+    };
+    if (tid == 0 && ntl) issue_tile(B.begin, tile_n(0), cur);
+    __syncthreads();
+    if (tid == 0) s_seg = B.seg;
+
+    for (uint32_t kt = 0; kt < ntl; ++kt, cur ^= 1, cs ^= 1) {
+      PH(0)
+      const uint32_t tn = tile_n(kt);
+      const bool full = tn == (uint32_t)T;
+      if (cur == 0) {
+        mbar_wait(&bar[0], ph0);
+        ph0 ^= 1u;
+      } else {
+        mbar_wait(&bar[1], ph1);
+        ph1 ^= 1u;
+      }
+      PH(1)
+      K* xk = bufk(cur);
+      V* xv = bufv(cur);
+      const K* ik = xk + s_off[cur][0];
+      const V* iv = xv + s_off[cur][1];
+
+      // ---- route + per-warp rank; records into registers ----
+      K key[IPT];
+      V val[IPT];
+      uint32_t bk[IPT], lr[IPT];
+      auto rank_one = [&](int i, uint32_t b) {
+        const uint32_t sh = (b & 1u) << 4;
+        const uint32_t old = atomicAdd(&mywh[b >> 1], 1u << sh);
+        bk[i] = b;
+        lr[i] = (old >> sh) & 0xffffu;
+      };
+      if (full && !(P.flags & PF_HEAVY)) {
+        const uint32_t shift = P.shift, mask = (1u << P.gamma) - 1u;
+        const bool ovf = (P.flags & PF_OVF) != 0;
+        const K thr = ovf ? P.ovf_thr : ~K(0);
+        const uint32_t ovfb = ovf ? nb - 1 : ((uint32_t)(~K(0) >> shift) & mask);
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          const uint32_t e = warp * WS + i * 32 + lane;
+          key[i] = ik[e];
+          if (VB) val[i] = iv[e];
+          rank_one(i, key[i] >= thr ? ovfb : ((uint32_t)(key[i] >> shift) & mask));
+          __syncwarp();
+        }
+      } else {
+        const Router<K> R = make_router<K>(P, hz, hk);
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          const uint32_t e = warp * WS + i * 32 + lane;
+          bk[i] = 0xFFFFu;
+          if (e < tn) {
+            key[i] = ik[e];
+            if (VB) val[i] = iv[e];
+            rank_one(i, R(key[i]));
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      PH(2)
+      // the other buffer (previous tile's staging) is free: stream the next tile
+      if (tid == 0) {
+        if (kt + 1 < ntl) issue_tile(B.begin + (uint64_t)(kt + 1) * T, tile_n(kt + 1), cur ^ 1);
+        pk[tn] = 0xFFFFFFFFu;  // order-check sentinel
+      }
+
+      // ---- bucket pair j = tid: prefix over warps; packed scan of
+      // (tile count | complete chunks of carry + run) ----
+      uint32_t s = 0, n0 = 0, n1 = 0, f0 = 0, f1 = 0;
+      uint2 I0 = make_uint2(0, 0), I1 = make_uint2(0, 0);
+      const uint2* cin = cst + cs * (TL::NBW + 1);
+      if ((uint32_t)tid < npair) {
+        I0 = cin[2 * tid];
+        if (2 * tid + 1 < nb) I1 = cin[2 * tid + 1];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const uint32_t x = wh[w * HW + tid];
+          wh[w * HW + tid] = s;
+          s += x;
+        }
+        n0 = s & 0xffffu;
+        n1 = s >> 16;
+        f0 = ((I0.x & 0xffffu) + n0) / C;
+        f1 = ((I1.x & 0xffffu) + n1) / C;
+      }
+      const uint32_t pv = (n0 + n1) | ((f0 + f1) << 16);
+      uint32_t incl = pv;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_wt[warp] = incl;
+      __syncthreads();
+      PH(3)
+      uint32_t nch;
+      {
+        uint32_t wp = lane < NW ? s_wt[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < NW; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULL, wp, o);
+          if (lane >= o) wp += y;
+        }
+        const uint32_t wex = __shfl_sync(FULL, wp, (warp + 31) & 31);
+        nch = __shfl_sync(FULL, wp, NW - 1) >> 16;  // chunks of the whole tile
+        const uint32_t ex = (warp ? wex : 0u) + incl - pv;
+        if ((uint32_t)tid < npair) {
+          const uint32_t t0 = ex & 0xffffu, c0 = ex >> 16;
+          binfo[2 * tid] = make_uint4(c0, I0.x, t0, I0.y);
+          binfo[2 * tid + 1] = make_uint4(c0 + f0, I1.x, t0 + n0, I1.y);
+          // next carry state and the copy that produces it
+          uint2* cout = cst + (cs ^ 1) * (TL::NBW + 1);
+          auto next = [&](uint32_t b, uint2 I, uint32_t n, uint32_t f, uint32_t t) {
+            const uint32_t cc = I.x & 0xffffu;
+            if (f == 0) {
+              bnf[b] = t | (cc << 16) | (n << 24);
+              cout[b] = make_uint2(I.x + n, I.y);
+            } else {
+              const uint32_t cnt = cc + n - f * C;
+              bnf[b] = (t + f * C - cc) | (cnt << 24);
+              cout[b] = make_uint2(cnt, I.y + f * C);
+            }
+          };
+          next(2 * tid, I0, n0, f0, t0);
+          if (2 * tid + 1 < nb) next(2 * tid + 1, I1, n1, f1, t0 + n0);
+          for (uint32_t k = 0; k < f0; ++k) cmap[c0 + k] = (uint16_t)(2 * tid);
+          for (uint32_t k = 0; k < f1; ++k) cmap[c0 + f0 + k] = (uint16_t)(2 * tid + 1);
+          // fold the tile offsets into this pair's per-warp prefixes
+          const uint32_t add = t0 | ((t0 + n0) << 16);
+#pragma unroll
+          for (int w = 0; w < NW; ++w) wh[w * HW + tid] += add;
+        }
+      }
+      __syncthreads();
+      PH(4)
+
+      // ---- placement into the staging area (this tile's buffer) ----
+#pragma unroll
+      for (int i = 0; i < IPT; ++i) {
+        if (full || bk[i] != 0xFFFFu) {
+          const uint32_t b = bk[i];
+          const uint32_t p = ((mywh[b >> 1] >> ((b & 1u) << 4)) & 0xffffu) + lr[i];
+          xk[p] = key[i];
+          if (VB) xv[p] = val[i];
+          pk[p] = (b << 16) | (warp * WS + i * 32 + lane);
+        }
+      }
+      __syncwarp();
+      for (uint32_t i = lane; i < HW; i += 32) mywh[i] = 0u;
+      __syncthreads();
+      PH(5)
+
+      // ---- stable order check (within a bucket, tile positions ascend) and
+      // write-out of every complete chunk: slot r of bucket b's current chunk
+      // run (carry slots [0, cc) first, then the staging run) ----
+      auto write_chunks = [&]() {
+        const uint32_t nslot = nch * C;
+        for (uint32_t q = tid; q < nslot; q += NT) {
+          const uint32_t g = q / C;
+          const uint32_t b = cmap[g];
+          const uint4 I = binfo[b];
+          const uint32_t r = (g - I.x) * C + (q % C);
+          const uint32_t cfill = I.y & 0xffffu;
+          if (r < (I.y >> 16)) continue;  // hole: the previous stripe's records
+          K kk;
+          V vv = V(0);
+          if (r < cfill) {
+            kk = ck[b * CP + r];
+            if (VB) vv = cv[b * CP + r];
+          } else {
+            const uint32_t p = I.z + r - cfill;
+            kk = xk[p];
+            if (VB) vv = xv[p];
+          }
+          const uint32_t d = I.w + r;
+          st_global(ko_seg + d, kk);
+          if (VB) st_global(vo_seg + d, vv);
+        }
+      };
+      {
+        bool bad = false;
+        for (uint32_t p = tid; p < tn; p += NT) {
+          const uint32_t wd = pk[p], nx = pk[p + 1];
+          bad |= ((wd ^ nx) < 65536u) & (nx < wd);
+        }
+        if (__any_sync(FULL, bad) && lane == 0) s_fix = 1u;
+      }
+      write_chunks();
+      __syncthreads();
+      PH(6)
+      if (s_fix || DTS_FORCE_FIXUP) {
+#if DTS_PHASE_PROF
+        if (tid == 0 && s_fix) atomicAdd(&g_phase[13], 1ull);
+#endif
+        // re-sort each bucket run by tile position (insertion sort), then
+        // write the chunks again (same addresses, corrected values)
+        for (uint32_t p = tid; p < tn; p += NT) {
+          const uint32_t x = pk[p];
+          const bool leader = p == 0 || ((pk[p - 1] ^ x) >= 65536u);
+          if (leader && p + 1 < tn && ((pk[p + 1] ^ x) < 65536u)) {
+            uint32_t c = 2;
+            while (p + c < tn && ((pk[p + c] ^ x) < 65536u)) ++c;
+            for (uint32_t a = 1; a < c; ++a) {
+              const uint32_t xw = pk[p + a];
+              const K xk2 = xk[p + a];
+              V xv2 = V(0);
+              if (VB) xv2 = xv[p + a];
+              uint32_t b2 = a;
+              while (b2 > 0 && pk[p + b2 - 1] > xw) {
+                pk[p + b2] = pk[p + b2 - 1];
+                xk[p + b2] = xk[p + b2 - 1];
+                if (VB) xv[p + b2] = xv[p + b2 - 1];
+                --b2;
+              }
+              pk[p + b2] = xw;
+              xk[p + b2] = xk2;
+              if (VB) xv[p + b2] = xv2;
+            }
+          }
+        }
+        __syncthreads();
+        write_chunks();
+        __syncthreads();
+        if (tid == 0) s_fix = 0u;
+      }
+
+      // ---- unfinished chunks become the carries: C lanes per bucket, one
+      // record each (32 / C buckets per warp step, 4 steps in flight) ----
+      {
+        constexpr uint32_t BPW = 32 / C;
+        constexpr uint32_t U = 4;
+        const uint32_t sub = lane / C, i = lane % C;
+        for (uint32_t b0 = warp * BPW; b0 < nb; b0 += NW * BPW * U) {
+          uint32_t dw[U];
+#pragma unroll
+          for (uint32_t u = 0; u < U; ++u) {
+            const uint32_t b = b0 + u * NW * BPW + sub;
+            dw[u] = b < nb ? bnf[b] : 0u;
+          }
+          K tk[U];
+          V tv[U];
+#pragma unroll
+          for (uint32_t u = 0; u < U; ++u) {
+            if (i < (dw[u] >> 24)) {
+              const uint32_t src = (dw[u] & 0xffffu) + i;
+              tk[u] = xk[src];
+              if (VB) tv[u] = xv[src];
+            }
+          }
+#pragma unroll
+          for (uint32_t u = 0; u < U; ++u) {
+            if (i < (dw[u] >> 24)) {
+              const uint32_t b = b0 + u * NW * BPW + sub;
+              const uint32_t dst = b * CP + ((dw[u] >> 16) & 0xffu) + i;
+              ck[dst] = tk[u];
+              if (VB) cv[dst] = tv[u];
+            }
+          }
+        }
+      }
+      PH(8)
+    }
+    // ---- stripe end: flush the unfinished chunks (partial sectors) ----
+    __syncthreads();
+    for (uint32_t b = tid; b < nb; b += NT) {
+      const uint2 I = cst[cs * (TL::NBW + 1) + b];
+      for (uint32_t r = I.x >> 16; r < (I.x & 0xffffu); ++r) {
+        st_global(ko_seg + I.y + r, ck[b * CP + r]);
+        if (VB) st_global(vo_seg + I.y + r, cv[b * CP + r]);
+      }
+    }
+  }
+  PH_DONE
+}
+
+}  // namespace dts

@@ -13,8 +13,13 @@ buf = (ctypes.c_ulonglong * 16)()
 g = torch.Generator(device="cuda"); g.manual_seed(0)
 src = torch.randint(0, 10**9, (n,), generator=g, device="cuda", dtype=torch.int64).to(torch.int32)
 k = torch.empty_like(src); v = torch.empty_like(src)
-names = ["top->issue", "issue->bar1", "tma wait", "rank", "prefix+scan", "tst", "placement",
-         "lookback", "bar(lookback)", "write-out"]
+import os
+if os.environ.get("DTS_WC", "1") != "0":
+    names = ["stripe/top", "tma wait", "rank", "pair scan", "binfo+map", "placement",
+             "check+write-out", "-", "carry", "-"]
+else:
+    names = ["top->issue", "issue->bar1", "tma wait", "rank", "prefix+scan", "tst", "placement",
+             "lookback", "bar(lookback)", "write-out"]
 for rep in range(2):
     k.copy_(src); torch.arange(n, out=v); torch.cuda.synchronize()
     L.dts_debug_phases(buf, 16, 1)
@@ -24,7 +29,7 @@ for rep in range(2):
 tiles = r.kernel_records["scatter"] / 4608.0
 ctas = buf[14]
 tot = sum(buf[i] for i in range(10))
-print(f"tiles ~{tiles:.0f}  CTA-runs {ctas}  spins {buf[15]}")
+print(f"tiles ~{tiles:.0f}  CTA-runs {ctas}  spins {buf[15]}  order-fixes wc {buf[13]} lookback {buf[12]}")
 for i, nm in enumerate(names):
     print(f"{nm:16s} {buf[i]/tiles:9.0f} cycles/tile  {100*buf[i]/tot:5.1f}%")
 print(f"{'total':16s} {tot/tiles:9.0f} cycles/tile")
