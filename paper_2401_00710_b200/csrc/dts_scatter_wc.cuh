@@ -43,12 +43,12 @@ template <typename K, int VB> struct WcSmem {
   static constexpr size_t ck = a16(pk + (size_t)(TL::T + 1) * 4);    // carry keys
   static constexpr size_t cv = a16(ck + (size_t)TL::NBW * TL::CP * sizeof(K));
   static constexpr size_t wh = a16(cv + (size_t)TL::NBW * TL::CP * VB);  // per-warp counters
-  // per bucket: {chunk offset, carry fill | hole << 16, tile offset, chunk base}
-  static constexpr size_t bi = a16(wh + (size_t)TL::NW * (TL::NBW / 2) * 4);
-  static constexpr size_t nf = a16(bi + (size_t)(TL::NBW + 1) * 16);  // tile count | chunks << 16
+  // per chunk of the tile: {dest of slot 0, staging index of slot 0,
+  // carry slots | hole << 8, bucket}
+  static constexpr size_t cd = a16(wh + (size_t)TL::NW * (TL::NBW / 2) * 4);
+  static constexpr size_t nf = a16(cd + (size_t)TL::MAXCH * 16);       // carry copy descriptors
   static constexpr size_t cst = a16(nf + (size_t)TL::NBW * 4);         // 2 x carry state
-  static constexpr size_t map = a16(cst + (size_t)2 * (TL::NBW + 1) * 8);  // chunk -> bucket
-  static constexpr size_t hk = a16(map + (size_t)TL::MAXCH * 2);
+  static constexpr size_t hk = a16(cst + (size_t)2 * (TL::NBW + 1) * 8);
   static constexpr size_t hz = a16(hk + (size_t)TL::HKC * sizeof(K));
   static constexpr size_t plan = a16(hz + (size_t)TL::HZC * 4);
   static constexpr size_t bar = a16(plan + sizeof(SegPlan));
@@ -95,10 +95,9 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
   K* ck = reinterpret_cast<K*>(smem_raw + SL::ck);
   V* cv = reinterpret_cast<V*>(smem_raw + SL::cv);
   uint32_t* wh = reinterpret_cast<uint32_t*>(smem_raw + SL::wh);
-  uint4* binfo = reinterpret_cast<uint4*>(smem_raw + SL::bi);
+  uint4* cdesc = reinterpret_cast<uint4*>(smem_raw + SL::cd);
   uint32_t* bnf = reinterpret_cast<uint32_t*>(smem_raw + SL::nf);  // copy: src | dst<<16 | cnt<<24
   uint2* cst = reinterpret_cast<uint2*>(smem_raw + SL::cst);      // {fill | hole << 16, chunk base}
-  uint16_t* cmap = reinterpret_cast<uint16_t*>(smem_raw + SL::map);
   K* hk = reinterpret_cast<K*>(smem_raw + SL::hk);
   uint32_t* hz = reinterpret_cast<uint32_t*>(smem_raw + SL::hz);
   SegPlan* splan = reinterpret_cast<SegPlan*>(smem_raw + SL::plan);
@@ -165,7 +164,7 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       for (uint32_t i = tid; i < P.nheavy && i < (uint32_t)TL::HKC; i += NT) hk[i] = heavy_pool[P.heavy_base + i];
     }
     // per bucket: block offset -> chunk base, hole = fill (carry state kept
-    // in binfo.y = fill | hole << 16 and binfo.w = chunk base across tiles)
+    // in cst = {fill | hole << 16, chunk base}, double-buffered across tiles)
     int cs = 0;  // carry-state buffer of the next tile
     for (uint32_t b = tid; b < nb; b += NT) {
       const uint32_t o = (uint32_t)(scan[P.cnt_base + (uint64_t)b * P.nrows + B.row] - P.scanbase);
@@ -288,8 +287,6 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
         const uint32_t ex = (warp ? wex : 0u) + incl - pv;
         if ((uint32_t)tid < npair) {
           const uint32_t t0 = ex & 0xffffu, c0 = ex >> 16;
-          binfo[2 * tid] = make_uint4(c0, I0.x, t0, I0.y);
-          binfo[2 * tid + 1] = make_uint4(c0 + f0, I1.x, t0 + n0, I1.y);
           // next carry state and the copy that produces it
           uint2* cout = cst + (cs ^ 1) * (TL::NBW + 1);
           auto next = [&](uint32_t b, uint2 I, uint32_t n, uint32_t f, uint32_t t) {
@@ -305,12 +302,21 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
           };
           next(2 * tid, I0, n0, f0, t0);
           if (2 * tid + 1 < nb) next(2 * tid + 1, I1, n1, f1, t0 + n0);
-          for (uint32_t k = 0; k < f0; ++k) cmap[c0 + k] = (uint16_t)(2 * tid);
-          for (uint32_t k = 0; k < f1; ++k) cmap[c0 + f0 + k] = (uint16_t)(2 * tid + 1);
+          // descriptors of this pair's complete chunks
+          auto chunks = [&](uint32_t b, uint2 I, uint32_t f, uint32_t t, uint32_t g0) {
+            const uint32_t cc = I.x & 0xffffu, ch = I.x >> 16;
+            for (uint32_t k = 0; k < f; ++k)
+              cdesc[g0 + k] = make_uint4(I.y + k * C, t - cc + k * C, k ? 0u : (cc | (ch << 8)), b);
+          };
+          chunks(2 * tid, I0, f0, t0, c0);
+          if (2 * tid + 1 < nb) chunks(2 * tid + 1, I1, f1, t0 + n0, c0 + f0);
           // fold the tile offsets into this pair's per-warp prefixes
           const uint32_t add = t0 | ((t0 + n0) << 16);
+          uint32_t hv[NW];
 #pragma unroll
-          for (int w = 0; w < NW; ++w) wh[w * HW + tid] += add;
+          for (int w = 0; w < NW; ++w) hv[w] = wh[w * HW + tid];
+#pragma unroll
+          for (int w = 0; w < NW; ++w) wh[w * HW + tid] = hv[w] + add;
         }
       }
       __syncthreads();
@@ -338,23 +344,19 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       auto write_chunks = [&]() {
         const uint32_t nslot = nch * C;
         for (uint32_t q = tid; q < nslot; q += NT) {
-          const uint32_t g = q / C;
-          const uint32_t b = cmap[g];
-          const uint4 I = binfo[b];
-          const uint32_t r = (g - I.x) * C + (q % C);
-          const uint32_t cfill = I.y & 0xffffu;
-          if (r < (I.y >> 16)) continue;  // hole: the previous stripe's records
+          const uint4 D = cdesc[q / C];
+          const uint32_t r = q % C;
+          if (r < ((D.z >> 8) & 0xffu)) continue;  // hole: the previous stripe's records
           K kk;
           V vv = V(0);
-          if (r < cfill) {
-            kk = ck[b * CP + r];
-            if (VB) vv = cv[b * CP + r];
+          if (r < (D.z & 0xffu)) {
+            kk = ck[D.w * CP + r];
+            if (VB) vv = cv[D.w * CP + r];
           } else {
-            const uint32_t p = I.z + r - cfill;
-            kk = xk[p];
-            if (VB) vv = xv[p];
+            kk = xk[D.y + r];
+            if (VB) vv = xv[D.y + r];
           }
-          const uint32_t d = I.w + r;
+          const uint32_t d = D.x + r;
           st_global(ko_seg + d, kk);
           if (VB) st_global(vo_seg + d, vv);
         }
