@@ -57,7 +57,6 @@ inline uint64_t block_records(int kb, int vb) { return scatter_T(kb, vb) * 8; }
 // write-combining scatter: stripe (= count-matrix row) of WC_LBS tiles
 constexpr uint64_t WC_LBS = 64;
 constexpr uint32_t COPY_CHUNK = 1u << 16;
-constexpr uint64_t SPAN_BATCH = 1u << 18;      // spans per k_local_sort launch
 constexpr uint64_t SAMPLE_FACTOR = 2;          // sample iff n' >= 2|S| (dtsort.py:225)
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -265,6 +264,7 @@ struct Sorter {
   dts_report* rep;
   Timer& tm;
   cudaStream_t st;
+  cudaEvent_t ev_cls = nullptr;  // after k_classify's read-back of a wave
 
   int cap;        // local-sort capacity (records)
   uint64_t thr;   // base-case threshold (records <= thr -> k_local_sort)
@@ -327,34 +327,37 @@ struct Sorter {
     }
   }
 
+  // Host-built spans/copies (the whole-input base case): copy the lists and
+  // their counts to the device and launch.
   int launch_spans_and_copies() {
     flush_span();
     if (spans.empty() && copies.empty()) return 0;
     const size_t sb = spans.size() * sizeof(Span), cb = copies.size() * sizeof(CopyR);
-    DTS_TRY(g_pin_span.ensure(sb + cb + 512));
+    DTS_TRY(g_pin_span.ensure(512 + align256(sb) + cb + 512));
     char* hp = (char*)g_pin_span.p;
-    std::memcpy(hp, spans.data(), sb);
-    std::memcpy(hp + align256(sb), copies.data(), cb);
-    // device copies of the descriptors live at the top of the meta region
+    uint32_t* hcnt = (uint32_t*)hp;
+    hcnt[0] = (uint32_t)spans.size();
+    hcnt[1] = (uint32_t)copies.size();
+    std::memcpy(hp + 512, spans.data(), sb);
+    std::memcpy(hp + 512 + align256(sb), copies.data(), cb);
     size_t save = meta.off;
-    Span* dsp = (Span*)meta.take(std::min<size_t>(spans.size(), SPAN_BATCH) * sizeof(Span) + 16);
-    CopyR* dcp = (CopyR*)meta.take(std::min<size_t>(copies.size(), SPAN_BATCH) * sizeof(CopyR) + 16);
-    if (!dsp || !dcp) return fail(DTS_ENOMEM, "workspace too small for span descriptors");
-    for (size_t s0 = 0; s0 < spans.size(); s0 += SPAN_BATCH) {
-      const size_t cnt = std::min<size_t>(SPAN_BATCH, spans.size() - s0);
-      CUDA_TRY(cudaMemcpyAsync(dsp, hp + s0 * sizeof(Span), cnt * sizeof(Span),
-                               cudaMemcpyHostToDevice, st));
-      uint64_t recs = 0;
-      for (size_t i = s0; i < s0 + cnt; ++i) recs += spans[i].len;
+    uint32_t* dcnt = (uint32_t*)meta.take(16);
+    Span* dsp = (Span*)meta.take(std::max<size_t>(1, spans.size()) * sizeof(Span));
+    CopyR* dcp = (CopyR*)meta.take(std::max<size_t>(1, copies.size()) * sizeof(CopyR));
+    if (!dcnt || !dsp || !dcp) return fail(DTS_ENOMEM, "workspace too small for span descriptors");
+    CUDA_TRY(cudaMemcpyAsync(dcnt, hp, 8, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dsp, hp + 512, sb, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dcp, hp + 512 + align256(sb), cb, cudaMemcpyHostToDevice, st));
+    uint64_t recs = 0;
+    for (const Span& x : spans) recs += x.len;
+    if (!spans.empty()) {
       Timer::Ev ev;
       tm.begin(DTS_K_LOCAL, ev);
-      {
-        auto fn = k_local_sort<K, VB>;
-        const size_t sm = LocalSmem<K, VB>::total;
-        DTS_TRY(set_smem(fn, sm));
-        const int grid = persistent_grid(fn, LocalTile<K, VB>::NT, sm, (uint32_t)cnt);
-        fn<<<grid, LocalTile<K, VB>::NT, sm, st>>>(dsp, (uint32_t)cnt, Ak, Av, Tk, Tv);
-      }
+      auto fn = k_local_sort<K, VB>;
+      const size_t sm = LocalSmem<K, VB>::total;
+      DTS_TRY(set_smem(fn, sm));
+      const int grid = persistent_grid(fn, LocalTile<K, VB>::NT, sm, (uint32_t)spans.size());
+      fn<<<grid, LocalTile<K, VB>::NT, sm, st>>>(dsp, dcnt, Ak, Av, Tk, Tv);
       tm.end(ev, recs);
       DTS_TRY(check_launch("k_local_sort"));
       if (rep) {
@@ -362,19 +365,19 @@ struct Sorter {
         rep->moves += recs;
       }
     }
-    for (size_t c0 = 0; c0 < copies.size(); c0 += SPAN_BATCH) {
-      const size_t cnt = std::min<size_t>(SPAN_BATCH, copies.size() - c0);
-      CUDA_TRY(cudaMemcpyAsync(dcp, hp + align256(sb) + c0 * sizeof(CopyR), cnt * sizeof(CopyR),
-                               cudaMemcpyHostToDevice, st));
-      uint64_t recs = 0;
-      for (size_t i = c0; i < c0 + cnt; ++i) recs += copies[i].len;
+    if (!copies.empty()) {
+      uint64_t crecs = 0;
+      for (const CopyR& x : copies) crecs += x.len;
       Timer::Ev ev;
       tm.begin(DTS_K_COPY, ev);
-      k_copy_ranges<K, VB><<<(unsigned)cnt, 256, 0, st>>>(dcp, Ak, Av, Tk, Tv);
-      tm.end(ev, recs);
+      k_copy_ranges<K, VB><<<(unsigned)std::min<size_t>(copies.size(), device_sms() * 4), 256, 0, st>>>(
+          dcp, dcnt + 1, Ak, Av, Tk, Tv);
+      tm.end(ev, crecs);
       DTS_TRY(check_launch("k_copy_ranges"));
-      if (rep) rep->moves += recs;
+      if (rep) rep->moves += crecs;
     }
+    // the pinned staging is reused: make sure the copies above have landed
+    CUDA_TRY(cudaStreamSynchronize(st));
     meta.off = save;
     spans.clear();
     copies.clear();
@@ -623,76 +626,87 @@ struct Sorter {
       tm.end(ev, wave_recs);
       DTS_TRY(check_launch("k_scatter"));
     }
-    // ---- read back ----
-    const double t_launch = trace_on() ? now_us() : 0.0;
-    DTS_TRY(g_pin_back.ensure(align256(pb) + align256(bs_total * 8) + bs_total + 256));
-    char* bp = (char*)g_pin_back.p;
-    CUDA_TRY(cudaMemcpyAsync(bp, dplans, pb, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(bp + align256(pb), dbs, bs_total * 8, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(bp + align256(pb) + align256(bs_total * 8), dkinds, bs_total,
-                             cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    const double t_sync = trace_on() ? now_us() : 0.0;
-    tm.harvest();
-    meta.off = save;
-    const SegPlan* rp = (const SegPlan*)bp;
-    const uint64_t* rbs = (const uint64_t*)(bp + align256(pb));
-    const uint8_t* rk = (const uint8_t*)(bp + align256(pb) + align256(bs_total * 8));
-
-    // ---- classify buckets (dtsort.py:244-318 _children_step) ----
+    // ---- classify buckets on the device (dtsort.py:244-318 _children_step),
+    // then the base case and the copies straight away; only the counters,
+    // the (few) next-level segments and the plans come back ----
     const uint32_t out_src = in_T ? 0u : 1u;  // where the scatter wrote
+    const uint64_t cap_copy = bs_total + wave_recs / COPY_CHUNK + 1;
+    Span* dspan = (Span*)meta.take(std::max<uint64_t>(1, bs_total) * sizeof(Span));
+    CopyR* dcopy = (CopyR*)meta.take(cap_copy * sizeof(CopyR));
+    NextSeg* dnext = (NextSeg*)meta.take(std::max<uint64_t>(1, bs_total) * sizeof(NextSeg));
+    unsigned long long* dcc = (unsigned long long*)meta.take(8 * sizeof(unsigned long long));
+    if (!dspan || !dcopy || !dnext || !dcc) return fail(DTS_ENOMEM, "workspace too small for level metadata");
+    CUDA_TRY(cudaMemsetAsync(dcc, 0, 8 * sizeof(unsigned long long), st));
+    k_classify<<<(unsigned)ns, 32, 0, st>>>(dplans, dbs, dkinds, (uint32_t)W, out_src, thr, COPY_CHUNK,
+                                           dspan, dcopy, dnext, dcc);
+    tm.launches += 1;
+    DTS_TRY(check_launch("k_classify"));
+    constexpr uint64_t NEXT_CAP = 4096;  // next segments returned with the counters
+    const uint64_t ncap = std::min<uint64_t>(NEXT_CAP, std::max<uint64_t>(1, bs_total));
+    DTS_TRY(g_pin_back.ensure(256 + align256(pb) + ncap * sizeof(NextSeg) + 256));
+    char* bp = (char*)g_pin_back.p;
+    CUDA_TRY(cudaMemcpyAsync(bp, dcc, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(bp + 256, dplans, pb, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(bp + 256 + align256(pb), dnext, ncap * sizeof(NextSeg),
+                             cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(ev_cls, st));
+    {
+      Timer::Ev ev;
+      tm.begin(DTS_K_LOCAL, ev);
+      auto fn = k_local_sort<K, VB>;
+      const size_t sm = LocalSmem<K, VB>::total;
+      DTS_TRY(set_smem(fn, sm));
+      const int grid = persistent_grid(fn, LocalTile<K, VB>::NT, sm, 1u << 30);
+      fn<<<grid, LocalTile<K, VB>::NT, sm, st>>>(dspan, reinterpret_cast<const uint32_t*>(dcc), Ak, Av, Tk, Tv);
+      tm.end(ev, 0);
+      DTS_TRY(check_launch("k_local_sort"));
+    }
+    if (out_src == 1) {
+      Timer::Ev ev;
+      tm.begin(DTS_K_COPY, ev);
+      k_copy_ranges<K, VB><<<(unsigned)(device_sms() * 4), 256, 0, st>>>(
+          dcopy, reinterpret_cast<const uint32_t*>(dcc + 1), Ak, Av, Tk, Tv);
+      tm.end(ev, 0);
+      DTS_TRY(check_launch("k_copy_ranges"));
+    }
+    const double t_launch = trace_on() ? now_us() : 0.0;
+    CUDA_TRY(cudaEventSynchronize(ev_cls));  // the base case keeps the GPU busy meanwhile
+    const double t_sync = trace_on() ? now_us() : 0.0;
+    const unsigned long long* hc = (const unsigned long long*)bp;
+    const SegPlan* rp = (const SegPlan*)(bp + 256);
+    const uint64_t nsp = hc[0] & 0xffffffffull, ncp = hc[1] & 0xffffffffull, nnx = hc[2] & 0xffffffffull;
+    std::vector<NextSeg> nx(nnx);
+    if (nnx <= ncap) {
+      if (nnx) std::memcpy(nx.data(), bp + 256 + align256(pb), nnx * sizeof(NextSeg));
+    } else {
+      CUDA_TRY(cudaMemcpy(nx.data(), dnext, nnx * sizeof(NextSeg), cudaMemcpyDeviceToHost));
+    }
+    std::sort(nx.begin(), nx.end(), [](const NextSeg& x, const NextSeg& y) { return x.offset < y.offset; });
+    for (const NextSeg& q : nx) next.push_back(HostSeg{q.offset, q.len, q.consumed, false});
     if (rep) {
-      rep->moves += wave_recs;
+      rep->moves += wave_recs + hc[6] + hc[7];
       rep->records_distributed += wave_recs;
       rep->levels = std::max(rep->levels, level + 1);
+      if (level + 1 < 64) rep->level_mass[level + 1] += hc[4];
+      if (level < 64) rep->heavy_records_removed[level] += hc[5];
+      rep->base_case_records += hc[6];
+      rep->kernel_records[DTS_K_LOCAL] += hc[6];
+      rep->kernel_records[DTS_K_COPY] += hc[7];
+      if (level == 0)
+        for (size_t i = 0; i < ns; ++i)
+          if (rp[i].flags & PF_OVF) rep->skipped_bits = (int32_t)(W - (rp[i].shift + rp[i].gamma));
     }
-    for (size_t i = 0; i < ns; ++i) {
-      const SegPlan& P = rp[i];
-      if (rep && level == 0 && (P.flags & PF_OVF))
-        rep->skipped_bits = (int32_t)(W - (P.shift + P.gamma));
-      const uint64_t* bs = rbs + P.bs_base;
-      const uint8_t* kd = rk + P.bs_base;
-      for (uint32_t b = 0; b < P.nb; ++b) {
-        const uint64_t lo = P.offset + bs[b], hi = P.offset + bs[b + 1];
-        if (hi <= lo) continue;
-        const uint64_t sz = hi - lo;
-        const uint8_t kind = kd[b];
-        const uint32_t rem = kind == KIND_OVF ? (uint32_t)W : (kind == KIND_HEAVY ? 0u : P.shift);
-        if (rem == 0) {
-          if (rep && kind == KIND_HEAVY && level < 64) rep->heavy_records_removed[level] += sz;
-          if (out_src == 1) {
-            if (sz <= thr) add_span(lo, sz, 1);
-            else {
-              flush_span();
-              add_copy(lo, sz);
-            }
-          } else {
-            flush_span();
-          }
-          continue;
-        }
-        if (rep && level + 1 < 64) rep->level_mass[level + 1] += sz;
-        if (sz <= thr) {
-          add_span(lo, sz, out_src);
-        } else {
-          flush_span();
-          next.push_back(HostSeg{lo, sz, (uint32_t)W - rem, false});
-        }
-      }
-    }
+    meta.off = save;
     if (trace_on()) {
-      const double t_cls = now_us();
-      const size_t nsp = spans.size() + (have_cur ? 1 : 0), ncp = copies.size();
-      const int rc = launch_spans_and_copies();
       std::fprintf(stderr,
-                   "[dts] level %d segs %zu recs %llu blks %zu tiles %llu sampled %zu | plan+launch %.0f us, "
-                   "gpu wait %.0f us, classify %.0f us, spans %zu copies %zu next %zu, span launch %.0f us\n",
+                   "[dts] level %d segs %zu recs %llu blks %zu tiles %llu sampled %zu wc %d | plan+launch %.0f us, "
+                   "wait %.0f us, spans %llu copies %llu next %llu, host %.0f us\n",
                    level, ns, (unsigned long long)wave_recs, blks.size(), (unsigned long long)ntile,
-                   sampled.size(), t_launch - t_plan0, t_sync - t_launch, t_cls - t_sync, nsp, ncp,
-                   next.size(), now_us() - t_cls);
-      return rc;
+                   sampled.size(), (int)wc, t_launch - t_plan0, t_sync - t_launch,
+                   (unsigned long long)nsp, (unsigned long long)ncp, (unsigned long long)nnx,
+                   now_us() - t_sync);
     }
-    return launch_spans_and_copies();
+    return 0;
   }
 
   size_t wave_meta_bytes(const HostSeg& s) const {
@@ -784,12 +798,15 @@ int sort_impl(void* keys, void* vals, uint64_t n, void* ws, size_t wsb, const dt
   S.stride = n <= 2 ? 1 : ceil_log2_u64(n);
   S.gs_max = sizeof(K) == 4 ? 10 : 9;
   S.smax = sizeof(K) == 4 ? 32768 : 16384;
+  if (cudaEventCreateWithFlags(&S.ev_cls, cudaEventDisableTiming) != cudaSuccess)
+    return fail(DTS_ECUDA, "cudaEventCreate failed");
   int rc = S.run();
   if (rc == 0) {
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) rc = fail(DTS_ECUDA, std::string("sort: ") + cudaGetErrorString(e));
   }
   tm.harvest();
+  cudaEventDestroy(S.ev_cls);
   if (rep) rep->gpu_launches += tm.launches;
   return rc;
 }

@@ -360,18 +360,132 @@ __global__ void __launch_bounds__(256) k_bucket_bounds(const SegPlan* __restrict
 }
 
 // ---------------------------------------------------------------------------
-// k_copy_ranges: finished ranges T -> A (heavy runs, exhausted-digit runs).
+// k_copy_ranges: finished ranges T -> A (heavy runs, exhausted-digit runs);
+// persistent CTAs over a device-resident list (count in *ncopy).
 // ---------------------------------------------------------------------------
 template <typename K, int VB>
 __global__ void __launch_bounds__(256) k_copy_ranges(const CopyR* __restrict__ rs,
+                                                     const uint32_t* __restrict__ ncopy,
                                                      K* __restrict__ Ak,
                                                      typename ValOf<VB>::T* __restrict__ Av,
                                                      const K* __restrict__ Tk,
                                                      const typename ValOf<VB>::T* __restrict__ Tv) {
-  const CopyR r = rs[blockIdx.x];
-  for (uint32_t i = threadIdx.x; i < r.len; i += blockDim.x) {
-    Ak[r.offset + i] = Tk[r.offset + i];
-    if (VB) Av[r.offset + i] = Tv[r.offset + i];
+  const uint32_t nc = *ncopy;
+  for (uint32_t c = blockIdx.x; c < nc; c += gridDim.x) {
+    const CopyR r = rs[c];
+    for (uint32_t i = threadIdx.x; i < r.len; i += blockDim.x) {
+      Ak[r.offset + i] = Tk[r.offset + i];
+      if (VB) Av[r.offset + i] = Tv[r.offset + i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_classify: the reference's per-child decisions (dtsort.py:244-318
+// _children_step) on the device, one thread per segment over its buckets:
+//   * exhausted buckets (heavy keys, or no digit bits left) are finished —
+//     if they sit in T they are copied (or, when small, sorted-as-copied by a
+//     base-case span);
+//   * light buckets <= thr join the current base-case span (adjacent
+//     buckets of one source are batched up to thr records, dtsort.py:262-286);
+//   * larger light buckets become next-level segments.
+// Spans / copies / next segments are appended with one atomic per segment;
+// the level's counters go to ctr[4..8) (InstrumentReport fields).
+// ---------------------------------------------------------------------------
+struct NextSeg {
+  uint64_t offset, len;
+  uint32_t consumed, pad;
+};
+
+__global__ void __launch_bounds__(32) k_classify(const SegPlan* __restrict__ plans,
+                                                 const uint64_t* __restrict__ bs,
+                                                 const uint8_t* __restrict__ kinds, uint32_t W,
+                                                 uint32_t out_src, uint64_t thr, uint32_t copy_chunk,
+                                                 Span* __restrict__ spans, CopyR* __restrict__ copies,
+                                                 NextSeg* __restrict__ next,
+                                                 unsigned long long* __restrict__ ctr) {
+  if (threadIdx.x != 0) return;
+  const SegPlan P = plans[blockIdx.x];
+  const uint64_t* b0 = bs + P.bs_base;
+  const uint8_t* kd = kinds + P.bs_base;
+  // two passes: count, reserve, write
+  uint32_t nsp = 0, ncp = 0, nnx = 0;
+  unsigned long long light = 0, heavy = 0, spanrec = 0, copyrec = 0;
+  uint32_t base_sp = 0, base_cp = 0, base_nx = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    uint32_t isp = 0, icp = 0, inx = 0;
+    bool have = false;
+    Span cur{0, 0, 0};
+    auto flush = [&]() {
+      if (have && cur.len) {
+        if (pass) spans[base_sp + isp] = cur;
+        ++isp;
+      }
+      have = false;
+    };
+    auto add_span = [&](uint64_t lo, uint64_t sz, uint32_t src) {
+      if (!pass) spanrec += sz;
+      if (have && cur.src == src && cur.offset + cur.len == lo && cur.len + sz <= thr) {
+        cur.len += (uint32_t)sz;
+        return;
+      }
+      flush();
+      cur = Span{lo, (uint32_t)sz, src};
+      have = true;
+    };
+    for (uint32_t b = 0; b < P.nb; ++b) {
+      const uint64_t lo = P.offset + b0[b], hi = P.offset + b0[b + 1];
+      if (hi <= lo) continue;
+      const uint64_t sz = hi - lo;
+      const uint8_t kind = kd[b];
+      const uint32_t rem = kind == KIND_OVF ? W : (kind == KIND_HEAVY ? 0u : P.shift);
+      if (rem == 0) {
+        if (!pass && kind == KIND_HEAVY) heavy += sz;
+        if (out_src == 1) {
+          if (sz <= thr) {
+            add_span(lo, sz, 1);
+          } else {
+            flush();
+            for (uint64_t o = 0; o < sz; o += copy_chunk) {
+              if (pass) {
+                CopyR r;
+                r.offset = lo + o;
+                r.len = (uint32_t)(sz - o < copy_chunk ? sz - o : copy_chunk);
+                r.pad = 0;
+                copies[base_cp + icp] = r;
+              } else {
+                copyrec += (sz - o < copy_chunk ? sz - o : copy_chunk);
+              }
+              ++icp;
+            }
+          }
+        } else {
+          flush();
+        }
+        continue;
+      }
+      if (!pass) light += sz;
+      if (sz <= thr) {
+        add_span(lo, sz, out_src);
+      } else {
+        flush();
+        if (pass) next[base_nx + inx] = NextSeg{lo, sz, W - rem, 0u};
+        ++inx;
+      }
+    }
+    flush();
+    if (!pass) {
+      nsp = isp;
+      ncp = icp;
+      nnx = inx;
+      if (nsp) base_sp = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[0]), nsp);
+      if (ncp) base_cp = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[1]), ncp);
+      if (nnx) base_nx = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[2]), nnx);
+      if (light) atomicAdd(&ctr[4], light);
+      if (heavy) atomicAdd(&ctr[5], heavy);
+      if (spanrec) atomicAdd(&ctr[6], spanrec);
+      if (copyrec) atomicAdd(&ctr[7], copyrec);
+    }
   }
 }
 

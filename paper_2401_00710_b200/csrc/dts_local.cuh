@@ -57,7 +57,7 @@ struct SpanSlot {  // a span staged in one buffer
 // ---------------------------------------------------------------------------
 template <typename K, int VB>
 __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
-    k_local_sort(const Span* __restrict__ spans, uint32_t nspan, K* __restrict__ Ak,
+    k_local_sort(const Span* __restrict__ spans, const uint32_t* __restrict__ nspan_p, K* __restrict__ Ak,
                  typename ValOf<VB>::T* __restrict__ Av, const K* __restrict__ Tk,
                  const typename ValOf<VB>::T* __restrict__ Tv) {
   using V = typename ValOf<VB>::T;
@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
   };
 
   const uint32_t G = gridDim.x;
+  const uint32_t nspan = *nspan_p;  // device-resident count (k_classify)
   Span nextS;  // thread 0: descriptor of the span after the one in flight
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -112,6 +113,8 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
   __syncthreads();
   uint32_t ph0 = 0u, ph1 = 0u;
   int cur = 0;
+  constexpr bool ph_on = DTS_PHASE_PROF == 2;
+  PH_INIT
   for (uint32_t sidx = blockIdx.x; sidx < nspan; sidx += G, cur ^= 1) {
     // stream the next span into the other buffer (freed by the previous
     // iteration's final barrier); fetch the descriptor after it
@@ -119,6 +122,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
       if (sidx + G < nspan) issue(nextS, cur ^ 1);
       if (sidx + 2 * G < nspan) nextS = spans[sidx + 2 * G];
     }
+    PH(9)
     if (cur == 0) {
       mbar_wait(&bar[0], ph0);
       ph0 ^= 1u;
@@ -126,6 +130,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
       mbar_wait(&bar[1], ph1);
       ph1 ^= 1u;
     }
+    PH(0)
     const SpanSlot S = s_slot[cur];
     const uint32_t n = S.len;
     K* sk = reinterpret_cast<K*>(smem_raw + (cur ? SL::k1 : SL::k0)) + S.ko;
@@ -148,6 +153,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
     if (lane == 0) s_diff[warp] = diff;
     if (tid == 0) s_big = 0u;  // read only after the scan barrier below
     __syncthreads();
+    PH(1)
     diff = 0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) diff |= s_diff[w];
@@ -171,6 +177,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
       const uint32_t nbin = 1u << bits, mask = nbin - 1u, nwd = (nbin + 1) >> 1;
       for (uint32_t i = tid; i < nwd; i += NT) cnt[i] = 0u;
       __syncthreads();
+      PH(2)
 #pragma unroll
       for (int i = 0; i < IPT; ++i) {
         const uint32_t e = warp * WS + i * 32 + lane;
@@ -180,6 +187,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
         }
       }
       __syncthreads();
+      PH(3)
       // exclusive scan over the bins (thread-contiguous word ranges), and the
       // largest group
       const uint32_t wpt = (nwd + NT - 1) / NT;
@@ -201,6 +209,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
       if (lane == 31) s_wt[warp] = incl;
       if (lane == 0 && mx > (uint32_t)TL::FIXMAX) s_big = 1u;
       __syncthreads();
+      PH(4)
       uint32_t wp = lane < NW ? s_wt[lane] : 0u;
 #pragma unroll
       for (int o = 1; o < NW; o <<= 1) {
@@ -216,9 +225,11 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
         base += lo + (x >> 16);
       }
       __syncthreads();
+      PH(5)
       lsd = s_big != 0u;
       if (!lsd) {
         // atomic slots (arbitrary order inside a group of equal keys)
+        uint16_t* fidx = si16 + TL::CAP;  // final order (second half of si)
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
           const uint32_t e = warp * WS + i * 32 + lane;
@@ -230,36 +241,45 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
           }
         }
         __syncthreads();
-        // each group of equal keys back into input order
-        const uint32_t bpt = (nbin + NT - 1) / NT;
-        const uint32_t d0 = min(nbin, tid * bpt), d1 = min(nbin, d0 + bpt);
-        uint32_t start = 0;
-        if (d0 > 0 && d0 < d1) {
-          const uint32_t dp = d0 - 1;
-          start = (cnt[dp >> 1] >> ((dp & 1u) << 4)) & 0xffffu;
-        }
-        for (uint32_t d = d0; d < d1; ++d) {
-          const uint32_t end = (cnt[d >> 1] >> ((d & 1u) << 4)) & 0xffffu;
-          if (end - start >= 2u) {
-            for (uint32_t a = start + 1; a < end; ++a) {
-              const uint16_t x = si16[a];
-              uint32_t b = a;
-              while (b > start && si16[b - 1] > x) {
-                si16[b] = si16[b - 1];
-                --b;
-              }
-              si16[b] = x;
+        PH(6)
+        // stable position = group start + number of group members that
+        // precede the record in the input (groups hold <= FIXMAX records)
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          const uint32_t e = warp * WS + i * 32 + lane;
+          if (e < n) {
+            const uint32_t d = (uint32_t)key[i] & mask;
+            const uint32_t end = (cnt[d >> 1] >> ((d & 1u) << 4)) & 0xffffu;
+            const uint32_t dp = d - 1u;
+            const uint32_t start = d ? (cnt[dp >> 1] >> ((dp & 1u) << 4)) & 0xffffu : 0u;
+            // the first four group members branch-free (groups are ~1-2
+            // records here), the rest in a loop
+            uint32_t r = 0;
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q) {
+              const uint32_t x = start + q < end ? (uint32_t)si16[start + q] : 0xFFFFu;
+              r += x < e;
             }
+            for (uint32_t q = start + 4; q < end; ++q) r += (uint32_t)si16[q] < e;
+            fidx[start + r] = (uint16_t)e;
           }
-          start = end;
         }
+#if DTS_PHASE_PROF == 2
+        if (tid == 0) {
+          atomicAdd(&g_phase[11], (unsigned long long)bits);
+          atomicAdd(&g_phase[12], 1ull);
+          atomicAdd(&g_phase[13], (unsigned long long)n);
+        }
+#endif
         __syncthreads();
+        PH(7)
         for (uint32_t p = tid; p < n; p += NT) {
-          const uint32_t e = si16[p];
+          const uint32_t e = si16[TL::CAP + p];
           ok[p] = sk[e];
           if (VB) ov[p] = sv[e];
         }
         __syncthreads();
+        PH(8)
         continue;
       }
     }
@@ -370,6 +390,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
     }
     __syncthreads();
   }
+  PH_DONE
 }
 
 }  // namespace dts

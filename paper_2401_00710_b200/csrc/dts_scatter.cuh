@@ -112,18 +112,19 @@ __device__ __forceinline__ T* opaque_ptr(T* p) {
 #endif
 #if DTS_PHASE_PROF
 __device__ unsigned long long g_phase[16];
+// each kernel sets `ph_on` (DTS_PHASE_PROF == 1: scatter kernels, 2: local sort)
 #define PH_INIT unsigned long long ph_acc[10] = {0}; long long ph_t = clock64();
-#define PH(k)                                  \
-  if (tid == 0) {                              \
-    const long long now_ = clock64();          \
-    ph_acc[k] += (unsigned long long)(now_ - ph_t); \
-    ph_t = now_;                               \
+#define PH(k)                                         \
+  if (ph_on && tid == 0) {                            \
+    const long long now_ = clock64();                 \
+    ph_acc[k] += (unsigned long long)(now_ - ph_t);   \
+    ph_t = now_;                                      \
   }
-#define PH_SPIN if (tid < 512) atomicAdd(&g_phase[15], 1ull);
-#define PH_DONE                                                        \
-  if (tid == 0) {                                                      \
+#define PH_SPIN if (ph_on && tid < 512) atomicAdd(&g_phase[15], 1ull);
+#define PH_DONE                                                          \
+  if (ph_on && tid == 0) {                                               \
     for (int k_ = 0; k_ < 10; ++k_) atomicAdd(&g_phase[k_], ph_acc[k_]); \
-    atomicAdd(&g_phase[14], 1ull);                                     \
+    atomicAdd(&g_phase[14], 1ull);                                       \
   }
 #else
 #define PH_INIT
@@ -230,6 +231,7 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
   __syncthreads();
   uint32_t phase = 0u;
   int cur = 0;
+  constexpr bool ph_on = DTS_PHASE_PROF == 1;
   PH_INIT
 
   for (uint32_t t = blockIdx.x; t < ntile; t += gridDim.x, cur ^= 1) {

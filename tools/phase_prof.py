@@ -14,7 +14,10 @@ g = torch.Generator(device="cuda"); g.manual_seed(0)
 src = torch.randint(0, 10**9, (n,), generator=g, device="cuda", dtype=torch.int64).to(torch.int32)
 k = torch.empty_like(src); v = torch.empty_like(src)
 import os
-if os.environ.get("DTS_WC", "1") != "0":
+LOCAL = os.environ.get("DTS_PHASE", "1") == "2"
+if LOCAL:
+    names = ["tma wait", "keys+diff", "zero", "hist", "scan", "slots", "rank", "write-out", "-", "top"]
+elif os.environ.get("DTS_WC", "1") != "0":
     names = ["stripe/top", "tma wait", "rank", "pair scan", "binfo+map", "placement",
              "check+write-out", "-", "carry", "-"]
 else:
@@ -26,10 +29,13 @@ for rep in range(2):
     r = sort_device(k, v, SortConfig(), 0, report=True)
     torch.cuda.synchronize()
     L.dts_debug_phases(buf, 16, 0)
-tiles = r.kernel_records["scatter"] / 4608.0
+tiles = (r.kernel_records["local_sort"] / 4100.0) if LOCAL else (r.kernel_records["scatter"] / 4608.0)
 ctas = buf[14]
 tot = sum(buf[i] for i in range(10))
 print(f"tiles ~{tiles:.0f}  CTA-runs {ctas}  spins {buf[15]}  order-fixes wc {buf[13]} lookback {buf[12]}")
 for i, nm in enumerate(names):
     print(f"{nm:16s} {buf[i]/tiles:9.0f} cycles/tile  {100*buf[i]/tot:5.1f}%")
 print(f"{'total':16s} {tot/tiles:9.0f} cycles/tile")
+if LOCAL and buf[12]:
+    print(f"counting-path spans {buf[12]}, mean bits {buf[11]/buf[12]:.2f}, mean records {buf[13]/buf[12]:.0f}, "
+          f"rank-loop iterations per record {buf[10]/max(buf[13],1):.2f}")
