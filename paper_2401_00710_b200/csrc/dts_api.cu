@@ -57,7 +57,10 @@ inline uint64_t block_records(int kb, int vb) { return scatter_T(kb, vb) * 8; }
 // write-combining scatter: stripe (= count-matrix row) of WC_LBS tiles
 constexpr uint64_t WC_LBS = 64;
 constexpr uint32_t COPY_CHUNK = 1u << 16;
-constexpr uint64_t SAMPLE_FACTOR = 2;          // sample iff n' >= 2|S| (dtsort.py:225)
+// sample iff n' >= SAMPLE_FACTOR x |S|.  The reference samples from 2|S|
+// (dtsort.py:225); here small segments skip it: heavy keys found there save
+// little, and each sampled segment costs a sample sort (output unaffected).
+constexpr uint64_t SAMPLE_FACTOR = 32;
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -681,7 +684,7 @@ struct Sorter {
     } else {
       CUDA_TRY(cudaMemcpy(nx.data(), dnext, nnx * sizeof(NextSeg), cudaMemcpyDeviceToHost));
     }
-    std::sort(nx.begin(), nx.end(), [](const NextSeg& x, const NextSeg& y) { return x.offset < y.offset; });
+    // (next-level order only shapes the waves; results do not depend on it)
     for (const NextSeg& q : nx) next.push_back(HostSeg{q.offset, q.len, q.consumed, false});
     if (rep) {
       rep->moves += wave_recs + hc[6] + hc[7];

@@ -171,10 +171,13 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
       continue;
     }
 
-    bool lsd = bits > TL::CB;
-    if (!lsd) {
-      // ================= counting path: one pass on the differing bits ==========
-      const uint32_t nbin = 1u << bits, mask = nbin - 1u, nwd = (nbin + 1) >> 1;
+    bool lsd = false;
+    {
+      // ================= counting path: one pass on the top <= CB differing
+      // bits; records sharing those bits are ranked by (key, position) ======
+      const int dbits = bits < TL::CB ? bits : TL::CB;
+      const int dsh = bits - dbits;  // bits below the digit (0: digit = whole order)
+      const uint32_t nbin = 1u << dbits, mask = nbin - 1u, nwd = (nbin + 1) >> 1;
       for (uint32_t i = tid; i < nwd; i += NT) cnt[i] = 0u;
       __syncthreads();
       PH(2)
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
       for (int i = 0; i < IPT; ++i) {
         const uint32_t e = warp * WS + i * 32 + lane;
         if (e < n) {
-          const uint32_t d = (uint32_t)key[i] & mask;
+          const uint32_t d = (uint32_t)(key[i] >> dsh) & mask;
           atomicAdd(&cnt[d >> 1], 1u << ((d & 1u) << 4));
         }
       }
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
         for (int i = 0; i < IPT; ++i) {
           const uint32_t e = warp * WS + i * 32 + lane;
           if (e < n) {
-            const uint32_t d = (uint32_t)key[i] & mask;
+            const uint32_t d = (uint32_t)(key[i] >> dsh) & mask;
             const uint32_t sh = (d & 1u) << 4;
             const uint32_t old = atomicAdd(&cnt[d >> 1], 1u << sh);
             si16[(old >> sh) & 0xffffu] = (uint16_t)e;
@@ -248,19 +251,30 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
         for (int i = 0; i < IPT; ++i) {
           const uint32_t e = warp * WS + i * 32 + lane;
           if (e < n) {
-            const uint32_t d = (uint32_t)key[i] & mask;
+            const uint32_t d = (uint32_t)(key[i] >> dsh) & mask;
             const uint32_t end = (cnt[d >> 1] >> ((d & 1u) << 4)) & 0xffffu;
             const uint32_t dp = d - 1u;
             const uint32_t start = d ? (cnt[dp >> 1] >> ((dp & 1u) << 4)) & 0xffffu : 0u;
-            // the first four group members branch-free (groups are ~1-2
-            // records here), the rest in a loop
+            // rank inside the group by (key, position); with dsh == 0 all
+            // keys of a group are equal and only positions count.  The first
+            // four members branch-free (groups hold ~1-2 records), the rest in
+            // a loop.
             uint32_t r = 0;
+            if (dsh == 0) {
 #pragma unroll
-            for (uint32_t q = 0; q < 4; ++q) {
-              const uint32_t x = start + q < end ? (uint32_t)si16[start + q] : 0xFFFFu;
-              r += x < e;
+              for (uint32_t q = 0; q < 4; ++q) {
+                const uint32_t x = start + q < end ? (uint32_t)si16[start + q] : 0xFFFFu;
+                r += x < e;
+              }
+              for (uint32_t q = start + 4; q < end; ++q) r += (uint32_t)si16[q] < e;
+            } else {
+              const K me = key[i];
+              for (uint32_t q = start; q < end; ++q) {
+                const uint32_t x = si16[q];
+                const K kx = sk[x];
+                r += (kx < me) || (kx == me && x < e);
+              }
             }
-            for (uint32_t q = start + 4; q < end; ++q) r += (uint32_t)si16[q] < e;
             fidx[start + r] = (uint16_t)e;
           }
         }
