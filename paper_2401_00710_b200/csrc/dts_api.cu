@@ -229,11 +229,12 @@ size_t meta_bytes(uint64_t n) {
   return (size_t(64) << 20) + (size_t)(rows * 1024 * 12) + (size_t)(tiles * 1024 * 4);
 }
 
-struct HostSeg {
+struct HostSeg {  // same layout as the device's NextSeg (bulk-copied)
   uint64_t offset, len;
   uint32_t consumed;
-  bool root;
+  uint32_t root;
 };
+static_assert(sizeof(HostSeg) == sizeof(NextSeg), "HostSeg mirrors NextSeg");
 
 // Flat exclusive scan of `e` u32 counts into u64 offsets.
 int flat_scan(const uint32_t* cnt, uint64_t e, uint64_t* out, uint64_t* partial, Timer& tm) {
@@ -489,6 +490,7 @@ struct Sorter {
     const uint64_t TT = wc ? (uint64_t)WcTile<K, VB>::T : (uint64_t)ScatterTile<K, VB>::T;
     // ---- count-matrix shape and hist blocks ----
     std::vector<Blk> blks;
+    blks.reserve(ns + wave_recs / BR + 1);
     uint64_t cnt_total = 0, bs_total = 0;
     for (size_t i = 0; i < ns; ++i) {
       SegPlan& P = plans[i];
@@ -678,14 +680,15 @@ struct Sorter {
     const unsigned long long* hc = (const unsigned long long*)bp;
     const SegPlan* rp = (const SegPlan*)(bp + 256);
     const uint64_t nsp = hc[0] & 0xffffffffull, ncp = hc[1] & 0xffffffffull, nnx = hc[2] & 0xffffffffull;
-    std::vector<NextSeg> nx(nnx);
+    // (next-level order only shapes the waves; results do not depend on it;
+    // NextSeg.pad = 0 reads as root = false)
+    const size_t nx0 = next.size();
+    next.resize(nx0 + nnx);
     if (nnx <= ncap) {
-      if (nnx) std::memcpy(nx.data(), bp + 256 + align256(pb), nnx * sizeof(NextSeg));
+      if (nnx) std::memcpy(next.data() + nx0, bp + 256 + align256(pb), nnx * sizeof(NextSeg));
     } else {
-      CUDA_TRY(cudaMemcpy(nx.data(), dnext, nnx * sizeof(NextSeg), cudaMemcpyDeviceToHost));
+      CUDA_TRY(cudaMemcpy(next.data() + nx0, dnext, nnx * sizeof(NextSeg), cudaMemcpyDeviceToHost));
     }
-    // (next-level order only shapes the waves; results do not depend on it)
-    for (const NextSeg& q : nx) next.push_back(HostSeg{q.offset, q.len, q.consumed, false});
     if (rep) {
       rep->moves += wave_recs + hc[6] + hc[7];
       rep->records_distributed += wave_recs;
@@ -728,7 +731,7 @@ struct Sorter {
       add_span(0, n, 0);
       return launch_spans_and_copies();
     }
-    std::vector<HostSeg> segs{HostSeg{0, n, 0, true}};
+    std::vector<HostSeg> segs{HostSeg{0, n, 0, 1u}};
     if (rep) rep->level_mass[0] = n;
     int level = 0;
     bool in_T = false;

@@ -21,8 +21,9 @@
 namespace dts {
 
 template <typename K, int VB> struct WcTile {
-  static constexpr int NT = 512;
+  static constexpr int NT = 512;  // (1024 threads measured slower: per-bucket phases)
   static constexpr int NW = NT / 32;
+  static constexpr int PT = NT / 512;  // threads per bucket pair in the pair phases
   static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? 9 : 5;
   static constexpr int WS = 32 * IPT;
   static constexpr int T = NT * IPT;
@@ -88,7 +89,8 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
   constexpr int NT = TL::NT, NW = TL::NW, IPT = TL::IPT, WS = TL::WS, T = TL::T, C = TL::C,
                 CP = TL::CP;
   constexpr uint32_t HW = TL::NBW / 2;
-  static_assert(HW <= (uint32_t)NT, "one bucket pair per thread");
+  constexpr int PT = TL::PT, WPT = NW / PT;  // threads per bucket pair, warps per thread
+  static_assert(HW * PT <= (uint32_t)NT, "PT threads per bucket pair");
   static_assert(T < 65536, "packed u16 counts");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* pk = reinterpret_cast<uint32_t*>(smem_raw + SL::pk);
@@ -251,21 +253,38 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       uint32_t s = 0, n0 = 0, n1 = 0, f0 = 0, f1 = 0;
       uint2 I0 = make_uint2(0, 0), I1 = make_uint2(0, 0);
       const uint2* cin = cst + cs * (TL::NBW + 1);
-      if ((uint32_t)tid < npair) {
-        I0 = cin[2 * tid];
-        if (2 * tid + 1 < nb) I1 = cin[2 * tid + 1];
+      const uint32_t pj = tid / PT, pq = tid % PT;  // bucket pair, part of it
+      const bool own = pj < npair;
+      if (own) {
+        I0 = cin[2 * pj];
+        if (2 * pj + 1 < nb) I1 = cin[2 * pj + 1];
 #pragma unroll
-        for (int w = 0; w < NW; ++w) {
-          const uint32_t x = wh[w * HW + tid];
-          wh[w * HW + tid] = s;
+        for (int w = pq * WPT; w < (int)(pq + 1) * WPT; ++w) {
+          const uint32_t x = wh[w * HW + pj];
+          wh[w * HW + pj] = s;
           s += x;
         }
-        n0 = s & 0xffffu;
-        n1 = s >> 16;
+      }
+      // combine the PT parts of a pair (adjacent lanes)
+      uint32_t pex = s, tot = s;
+      if (PT > 1) {
+#pragma unroll
+        for (int o = 1; o < PT; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULL, pex, o);
+          if ((int)pq >= o) pex += y;
+        }
+        tot = __shfl_sync(FULL, pex, (lane | (PT - 1)));
+        pex -= s;  // exclusive over the parts
+      } else {
+        pex = 0u;
+      }
+      if (own) {
+        n0 = tot & 0xffffu;
+        n1 = tot >> 16;
         f0 = ((I0.x & 0xffffu) + n0) / C;
         f1 = ((I1.x & 0xffffu) + n1) / C;
       }
-      const uint32_t pv = (n0 + n1) | ((f0 + f1) << 16);
+      const uint32_t pv = (own && pq == PT - 1) ? ((n0 + n1) | ((f0 + f1) << 16)) : 0u;
       uint32_t incl = pv;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -286,7 +305,7 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
         const uint32_t wex = __shfl_sync(FULL, wp, (warp + 31) & 31);
         nch = __shfl_sync(FULL, wp, NW - 1) >> 16;  // chunks of the whole tile
         const uint32_t ex = (warp ? wex : 0u) + incl - pv;
-        if ((uint32_t)tid < npair) {
+        if (own) {
           const uint32_t t0 = ex & 0xffffu, c0 = ex >> 16;
           // next carry state and the copy that produces it
           uint2* cout = cst + (cs ^ 1) * (TL::NBW + 1);
@@ -301,23 +320,28 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
               cout[b] = make_uint2(cnt, I.y + f * C);
             }
           };
-          next(2 * tid, I0, n0, f0, t0);
-          if (2 * tid + 1 < nb) next(2 * tid + 1, I1, n1, f1, t0 + n0);
           // descriptors of this pair's complete chunks
           auto chunks = [&](uint32_t b, uint2 I, uint32_t f, uint32_t t, uint32_t g0) {
             const uint32_t cc = I.x & 0xffffu, ch = I.x >> 16;
             for (uint32_t k = 0; k < f; ++k)
               cdesc[g0 + k] = make_uint4(I.y + k * C, t - cc + k * C, k ? 0u : (cc | (ch << 8)), b);
           };
-          chunks(2 * tid, I0, f0, t0, c0);
-          if (2 * tid + 1 < nb) chunks(2 * tid + 1, I1, f1, t0 + n0, c0 + f0);
-          // fold the tile offsets into this pair's per-warp prefixes
-          const uint32_t add = t0 | ((t0 + n0) << 16);
-          uint32_t hv[NW];
+          if (pq == 0) {
+            next(2 * pj, I0, n0, f0, t0);
+            chunks(2 * pj, I0, f0, t0, c0);
+          }
+          if (pq == PT - 1 && 2 * pj + 1 < nb) {
+            next(2 * pj + 1, I1, n1, f1, t0 + n0);
+            chunks(2 * pj + 1, I1, f1, t0 + n0, c0 + f0);
+          }
+          // fold the tile offsets (and the earlier parts' counts) into this
+          // part's per-warp prefixes
+          const uint32_t add = (t0 | ((t0 + n0) << 16)) + pex;
+          uint32_t hv[WPT];
 #pragma unroll
-          for (int w = 0; w < NW; ++w) hv[w] = wh[w * HW + tid];
+          for (int w = 0; w < WPT; ++w) hv[w] = wh[(pq * WPT + w) * HW + pj];
 #pragma unroll
-          for (int w = 0; w < NW; ++w) wh[w * HW + tid] = hv[w] + add;
+          for (int w = 0; w < WPT; ++w) wh[(pq * WPT + w) * HW + pj] = hv[w] + add;
         }
       }
       __syncthreads();
