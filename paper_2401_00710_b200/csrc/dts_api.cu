@@ -642,7 +642,7 @@ struct Sorter {
     unsigned long long* dcc = (unsigned long long*)meta.take(8 * sizeof(unsigned long long));
     if (!dspan || !dcopy || !dnext || !dcc) return fail(DTS_ENOMEM, "workspace too small for level metadata");
     CUDA_TRY(cudaMemsetAsync(dcc, 0, 8 * sizeof(unsigned long long), st));
-    k_classify<<<(unsigned)ns, 32, 0, st>>>(dplans, dbs, dkinds, (uint32_t)W, out_src, thr, COPY_CHUNK,
+    k_classify<<<(unsigned)ns, CLS_NT, 0, st>>>(dplans, dbs, dkinds, (uint32_t)W, out_src, thr, COPY_CHUNK,
                                            dspan, dcopy, dnext, dcc);
     tm.launches += 1;
     DTS_TRY(check_launch("k_classify"));

@@ -397,94 +397,148 @@ struct NextSeg {
   uint32_t consumed, pad;
 };
 
-__global__ void __launch_bounds__(32) k_classify(const SegPlan* __restrict__ plans,
-                                                 const uint64_t* __restrict__ bs,
-                                                 const uint8_t* __restrict__ kinds, uint32_t W,
-                                                 uint32_t out_src, uint64_t thr, uint32_t copy_chunk,
-                                                 Span* __restrict__ spans, CopyR* __restrict__ copies,
-                                                 NextSeg* __restrict__ next,
-                                                 unsigned long long* __restrict__ ctr) {
-  if (threadIdx.x != 0) return;
+constexpr int CLS_NT = 256;
+constexpr int CLS_MAXB = 1032;  // buckets per segment handled in SMEM (nbmax + 1)
+
+__global__ void __launch_bounds__(CLS_NT) k_classify(const SegPlan* __restrict__ plans,
+                                                     const uint64_t* __restrict__ bs,
+                                                     const uint8_t* __restrict__ kinds, uint32_t W,
+                                                     uint32_t out_src, uint64_t thr, uint32_t copy_chunk,
+                                                     Span* __restrict__ spans, CopyR* __restrict__ copies,
+                                                     NextSeg* __restrict__ next,
+                                                     unsigned long long* __restrict__ ctr) {
+  enum : uint32_t { T_EMPTY = 0, T_CAND = 1, T_FLUSH = 2, T_COPY = 3, T_NEXT = 4 };
+  __shared__ uint64_t s_bs[CLS_MAXB];
+  __shared__ uint32_t s_ty[CLS_MAXB];
+  __shared__ Span s_sp[CLS_MAXB];
+  __shared__ uint32_t s_n[4];  // spans, copies, next, base slots
+  __shared__ unsigned long long s_acc[4];
+  __shared__ uint32_t s_base[3];
+  __shared__ uint32_t s_slow;
   const SegPlan P = plans[blockIdx.x];
-  const uint64_t* b0 = bs + P.bs_base;
-  const uint8_t* kd = kinds + P.bs_base;
-  // two passes: count, reserve, write
-  uint32_t nsp = 0, ncp = 0, nnx = 0;
-  unsigned long long light = 0, heavy = 0, spanrec = 0, copyrec = 0;
-  uint32_t base_sp = 0, base_cp = 0, base_nx = 0;
-  for (int pass = 0; pass < 2; ++pass) {
-    uint32_t isp = 0, icp = 0, inx = 0;
-    bool have = false;
-    Span cur{0, 0, 0};
-    auto flush = [&]() {
-      if (have && cur.len) {
-        if (pass) spans[base_sp + isp] = cur;
-        ++isp;
-      }
-      have = false;
-    };
-    auto add_span = [&](uint64_t lo, uint64_t sz, uint32_t src) {
-      if (!pass) spanrec += sz;
-      if (have && cur.src == src && cur.offset + cur.len == lo && cur.len + sz <= thr) {
-        cur.len += (uint32_t)sz;
-        return;
-      }
-      flush();
-      cur = Span{lo, (uint32_t)sz, src};
-      have = true;
-    };
-    for (uint32_t b = 0; b < P.nb; ++b) {
-      const uint64_t lo = P.offset + b0[b], hi = P.offset + b0[b + 1];
-      if (hi <= lo) continue;
-      const uint64_t sz = hi - lo;
-      const uint8_t kind = kd[b];
+  const uint32_t nb = P.nb;
+  if (threadIdx.x < 4) {
+    s_n[threadIdx.x] = 0;
+    s_acc[threadIdx.x] = 0;
+  }
+  if (threadIdx.x == 0) s_slow = 0u;
+  for (uint32_t b = threadIdx.x; b <= nb; b += CLS_NT) s_bs[b] = bs[P.bs_base + b];
+  __syncthreads();
+  // ---- per bucket: decision (parallel) ----
+  unsigned long long light = 0, heavy = 0, copyrec = 0;
+  for (uint32_t b = threadIdx.x; b < nb; b += CLS_NT) {
+    const uint64_t lo = s_bs[b], sz = s_bs[b + 1] - lo;
+    uint32_t ty = T_EMPTY;
+    if (sz) {
+      const uint8_t kind = kinds[P.bs_base + b];
       const uint32_t rem = kind == KIND_OVF ? W : (kind == KIND_HEAVY ? 0u : P.shift);
       if (rem == 0) {
-        if (!pass && kind == KIND_HEAVY) heavy += sz;
-        if (out_src == 1) {
-          if (sz <= thr) {
-            add_span(lo, sz, 1);
-          } else {
-            flush();
-            for (uint64_t o = 0; o < sz; o += copy_chunk) {
-              if (pass) {
-                CopyR r;
-                r.offset = lo + o;
-                r.len = (uint32_t)(sz - o < copy_chunk ? sz - o : copy_chunk);
-                r.pad = 0;
-                copies[base_cp + icp] = r;
-              } else {
-                copyrec += (sz - o < copy_chunk ? sz - o : copy_chunk);
-              }
-              ++icp;
-            }
-          }
-        } else {
-          flush();
-        }
-        continue;
-      }
-      if (!pass) light += sz;
-      if (sz <= thr) {
-        add_span(lo, sz, out_src);
+        if (kind == KIND_HEAVY) heavy += sz;
+        ty = out_src == 1 ? (sz <= thr ? T_CAND : T_COPY) : T_FLUSH;
       } else {
-        flush();
-        if (pass) next[base_nx + inx] = NextSeg{lo, sz, W - rem, 0u};
-        ++inx;
+        light += sz;
+        ty = sz <= thr ? T_CAND : T_NEXT;
+      }
+      if (ty == T_COPY) copyrec += sz;
+    }
+    s_ty[b] = ty;
+  }
+  if (light) atomicAdd(&s_acc[0], light);
+  if (heavy) atomicAdd(&s_acc[1], heavy);
+  if (copyrec) atomicAdd(&s_acc[2], copyrec);
+  __syncthreads();
+  // ---- spans: greedy packing of adjacent candidates.  When no two
+  // neighbouring candidates fit one span together (and no bucket is empty)
+  // every candidate is its own span: emitted in parallel; otherwise one
+  // thread walks the buckets. ----
+  for (uint32_t b = threadIdx.x; b < nb; b += CLS_NT) {
+    const uint32_t ty = s_ty[b];
+    if (ty == T_EMPTY) s_slow = 1u;
+    if (ty == T_CAND && b + 1 < nb && s_ty[b + 1] == T_CAND &&
+        (s_bs[b + 2] - s_bs[b]) <= thr)
+      s_slow = 1u;
+  }
+  __syncthreads();
+  if (!s_slow) {
+    unsigned long long rec = 0;
+    for (uint32_t b = threadIdx.x; b < nb; b += CLS_NT) {
+      if (s_ty[b] == T_CAND) {
+        const uint32_t sz = (uint32_t)(s_bs[b + 1] - s_bs[b]);
+        s_sp[atomicAdd(&s_n[0], 1u)] = Span{P.offset + s_bs[b], sz, out_src};
+        rec += sz;
       }
     }
-    flush();
-    if (!pass) {
-      nsp = isp;
-      ncp = icp;
-      nnx = inx;
-      if (nsp) base_sp = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[0]), nsp);
-      if (ncp) base_cp = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[1]), ncp);
-      if (nnx) base_nx = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[2]), nnx);
-      if (light) atomicAdd(&ctr[4], light);
-      if (heavy) atomicAdd(&ctr[5], heavy);
-      if (spanrec) atomicAdd(&ctr[6], spanrec);
-      if (copyrec) atomicAdd(&ctr[7], copyrec);
+    if (rec) atomicAdd(&s_acc[3], rec);
+  } else if (threadIdx.x == 0) {
+    uint32_t nsp = 0;
+    bool have = false;
+    Span cur{0, 0, 0};
+    unsigned long long spanrec = 0;
+    for (uint32_t b = 0; b < nb; ++b) {
+      const uint32_t ty = s_ty[b];
+      if (ty == T_EMPTY) continue;
+      if (ty == T_CAND) {
+        const uint64_t lo = P.offset + s_bs[b];
+        const uint32_t sz = (uint32_t)(s_bs[b + 1] - s_bs[b]);
+        spanrec += sz;
+        if (have && cur.offset + cur.len == lo && cur.len + sz <= thr) {
+          cur.len += sz;
+        } else {
+          if (have) s_sp[nsp++] = cur;
+          cur = Span{lo, sz, out_src};
+          have = true;
+        }
+      } else {
+        if (have) s_sp[nsp++] = cur;
+        have = false;
+      }
+    }
+    if (have) s_sp[nsp++] = cur;
+    s_n[0] = nsp;
+    s_acc[3] = spanrec;
+  }
+  // ---- copies (chunked) and next segments: counted per bucket ----
+  for (uint32_t b = threadIdx.x; b < nb; b += CLS_NT) {
+    const uint32_t ty = s_ty[b];
+    if (ty == T_COPY) {
+      const uint64_t sz = s_bs[b + 1] - s_bs[b];
+      atomicAdd(&s_n[1], (uint32_t)((sz + copy_chunk - 1) / copy_chunk));
+    } else if (ty == T_NEXT) {
+      atomicAdd(&s_n[2], 1u);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_base[0] = s_n[0] ? atomicAdd(reinterpret_cast<unsigned int*>(&ctr[0]), s_n[0]) : 0u;
+    s_base[1] = s_n[1] ? atomicAdd(reinterpret_cast<unsigned int*>(&ctr[1]), s_n[1]) : 0u;
+    s_base[2] = s_n[2] ? atomicAdd(reinterpret_cast<unsigned int*>(&ctr[2]), s_n[2]) : 0u;
+    if (s_acc[0]) atomicAdd(&ctr[4], s_acc[0]);
+    if (s_acc[1]) atomicAdd(&ctr[5], s_acc[1]);
+    if (s_acc[3]) atomicAdd(&ctr[6], s_acc[3]);
+    if (s_acc[2]) atomicAdd(&ctr[7], s_acc[2]);
+    s_n[1] = 0;
+    s_n[2] = 0;
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < s_n[0]; i += CLS_NT) spans[s_base[0] + i] = s_sp[i];
+  for (uint32_t b = threadIdx.x; b < nb; b += CLS_NT) {
+    const uint32_t ty = s_ty[b];
+    if (ty == T_COPY) {
+      const uint64_t lo = P.offset + s_bs[b], sz = s_bs[b + 1] - s_bs[b];
+      const uint32_t nc = (uint32_t)((sz + copy_chunk - 1) / copy_chunk);
+      const uint32_t at = s_base[1] + atomicAdd(&s_n[1], nc);
+      for (uint32_t c = 0; c < nc; ++c) {
+        CopyR r;
+        r.offset = lo + (uint64_t)c * copy_chunk;
+        r.len = (uint32_t)(sz - (uint64_t)c * copy_chunk < copy_chunk ? sz - (uint64_t)c * copy_chunk : copy_chunk);
+        r.pad = 0;
+        copies[at + c] = r;
+      }
+    } else if (ty == T_NEXT) {
+      const uint64_t lo = P.offset + s_bs[b], sz = s_bs[b + 1] - s_bs[b];
+      const uint8_t kind = kinds[P.bs_base + b];
+      const uint32_t rem = kind == KIND_OVF ? W : P.shift;
+      next[s_base[2] + atomicAdd(&s_n[2], 1u)] = NextSeg{lo, sz, W - rem, 0u};
     }
   }
 }
