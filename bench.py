@@ -304,15 +304,19 @@ def run_ours(args, cfgd, rank, world, local_rank):
         launches = int(sum(r.gpu_launches for r in reps))
         shares = {c: round(sum(r.kernel_ms[c] for r in reps) / (ms * args.steps), 4)
                   for c in reps[0].kernel_ms}
+        # ncu dram bytes of the scatter per record (profiles/traffic.json, one
+        # --set full capture) x records per launch of this run
         traffic = None
         try:
             with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-                traffic = json.load(f).get("k_scatter_bytes_per_launch")
+                bpr = json.load(f).get("dram_bytes_per_record")
+            if bpr:
+                traffic = int(bpr * sc_rec / max(sc_launch, 1))
         except Exception:
             pass
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "k_scatter", "peak_kind": peak_kind,
+                "kernel": "k_scatter_wc (write-combining scatter)", "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": int(per_launch_bytes),
                 "ms_per_launch": round(per_launch_ms, 4),
                 "step_share": shares}
