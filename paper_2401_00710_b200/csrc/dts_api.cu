@@ -563,8 +563,7 @@ struct Sorter {
       CUDA_TRY(cudaMemcpyAsync(dblk_tile0, htl + align256(tb), b0b, cudaMemcpyHostToDevice, st));
     }
     const bool sample_later = !sampled.empty() && !wc_env;
-    if (sampled.empty() || !sample_later || wc_env)
-      CUDA_TRY(cudaMemcpyAsync(dplans, hp, pb, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dplans, hp, pb, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(dblks, hp + align256(pb), bb, cudaMemcpyHostToDevice, st));
     if (sample_later) {
       // DTS_WC=0: plans (with the count-matrix shape) go up before sampling
