@@ -1161,6 +1161,9 @@ int dts_sort(void* keys, void* vals, uint64_t n, int kb, int vb, void* ws, size_
     return fail(DTS_EINVAL, "need 1 <= gamma_lo <= gamma_hi <= 16");
   if (rep) std::memset(rep, 0, sizeof(*rep));
   if (n == 0) return 0;
+  if (n >= (uint64_t(1) << 32))
+    return fail(DTS_EINVAL, "n must be < 2^32 per call (segment positions are 32-bit); shard larger "
+                            "inputs with distributed.dist_sort");
   if (wsb < dts_workspace_bytes(n, kb, vb))
     return fail(DTS_ENOMEM, "workspace holds " + std::to_string(wsb) + " bytes, need " +
                                 std::to_string(dts_workspace_bytes(n, kb, vb)));

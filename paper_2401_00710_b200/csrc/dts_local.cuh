@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
     if (blockIdx.x < nspan) issue(spans[blockIdx.x], 0);
     if (blockIdx.x + G < nspan) nextS = spans[blockIdx.x + G];
   }
+  for (uint32_t i = tid; i < (uint32_t)(SL::cnt_bytes / 4); i += NT) cnt[i] = 0u;
   __syncthreads();
   uint32_t ph0 = 0u, ph1 = 0u;
   int cur = 0;
@@ -178,8 +179,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
       const int dbits = bits < TL::CB ? bits : TL::CB;
       const int dsh = bits - dbits;  // bits below the digit (0: digit = whole order)
       const uint32_t nbin = 1u << dbits, mask = nbin - 1u, nwd = (nbin + 1) >> 1;
-      for (uint32_t i = tid; i < nwd; i += NT) cnt[i] = 0u;
-      __syncthreads();
+      // (the bins are zero here: zeroed at start and after every span)
       PH(2)
 #pragma unroll
       for (int i = 0; i < IPT; ++i) {
@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
           ok[p] = sk[e];
           if (VB) ov[p] = sv[e];
         }
+        for (uint32_t i = tid; i < nwd; i += NT) cnt[i] = 0u;  // ready for the next span
         __syncthreads();
         PH(8)
         continue;
@@ -402,6 +403,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
       ok[p] = sk[p];
       if (VB) ov[p] = sv[si[p] & 0xffffu];
     }
+    for (uint32_t i = tid; i < (uint32_t)(SL::cnt_bytes / 4); i += NT) cnt[i] = 0u;
     __syncthreads();
   }
   PH_DONE

@@ -66,3 +66,14 @@ def test_invalid_arguments_fail_before_touching_the_device():
     cfg.gamma_lo = 0
     rc = L.dts_sort(None, None, 10, 4, 4, None, 0, ctypes.byref(cfg), None, None)
     assert rc == -1 and b"NULL" in L.dts_last_error()
+
+
+def test_oversized_call_is_rejected_before_touching_the_device():
+    import ctypes
+
+    L = _lib.lib()
+    cfg = _lib.DtsConfig()
+    cfg.gamma_lo, cfg.gamma_hi = 8, 12
+    dummy = ctypes.c_void_p(16)
+    rc = L.dts_sort(dummy, None, 1 << 32, 4, 0, None, 0, ctypes.byref(cfg), None, None)
+    assert rc == -1 and b"2^32" in L.dts_last_error()
