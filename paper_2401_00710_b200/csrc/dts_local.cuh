@@ -107,6 +107,9 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
     fence_mbar_init();
     s_fix = 0u;
     s_big = 0u;
+  }
+  __syncthreads();
+  if (tid == NT - 1) {
     if (blockIdx.x < nspan) issue(spans[blockIdx.x], 0);
     if (blockIdx.x + G < nspan) nextS = spans[blockIdx.x + G];
   }
@@ -117,12 +120,6 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
   constexpr bool ph_on = DTS_PHASE_PROF == 2;
   PH_INIT
   for (uint32_t sidx = blockIdx.x; sidx < nspan; sidx += G, cur ^= 1) {
-    // stream the next span into the other buffer (freed by the previous
-    // iteration's final barrier); fetch the descriptor after it
-    if (tid == 0) {
-      if (sidx + G < nspan) issue(nextS, cur ^ 1);
-      if (sidx + 2 * G < nspan) nextS = spans[sidx + 2 * G];
-    }
     PH(9)
     if (cur == 0) {
       mbar_wait(&bar[0], ph0);
@@ -155,6 +152,13 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
     if (tid == 0) s_big = 0u;  // read only after the scan barrier below
     __syncthreads();
     PH(1)
+    // stream the next span into the other buffer (freed by the previous
+    // iteration's final barrier); fetch the descriptor after it.  Done by the
+    // last thread after the first barrier so no warp starts the span late.
+    if (tid == NT - 1) {
+      if (sidx + G < nspan) issue(nextS, cur ^ 1);
+      if (sidx + 2 * G < nspan) nextS = spans[sidx + 2 * G];
+    }
     diff = 0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) diff |= s_diff[w];
