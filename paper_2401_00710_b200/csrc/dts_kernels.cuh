@@ -12,6 +12,7 @@
 //   k_copy_ranges  : T -> A copies of finished ranges (dtsort.py:111-124)
 //   k_merge_*      : dovetail merge pieces (dtmerge.py:58-238)
 #pragma once
+#include <type_traits>
 #include "dts_common.cuh"
 
 namespace dts {
@@ -371,12 +372,31 @@ __global__ void __launch_bounds__(256) k_copy_ranges(const CopyR* __restrict__ r
                                                      const K* __restrict__ Tk,
                                                      const typename ValOf<VB>::T* __restrict__ Tv) {
   const uint32_t nc = *ncopy;
+  // one column: 16-byte vectors for the aligned body, elements at the ends
+  auto col = [&](auto* dst, const auto* src, uint64_t off, uint32_t len) {
+    using E = typename std::remove_const<typename std::remove_pointer<decltype(src)>::type>::type;
+    constexpr uint32_t VEC = 16 / sizeof(E);
+    const uint32_t head = (uint32_t)((VEC - (off % VEC)) % VEC) < len ? (uint32_t)((VEC - (off % VEC)) % VEC) : len;
+    const uint32_t nv = (len - head) / VEC;
+    for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) dst[off + i] = src[off + i];
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + off + head);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + off + head);
+    constexpr uint32_t U = 4;  // 4 vectors in flight per thread
+    uint32_t i = threadIdx.x;
+    for (; i + (U - 1) * blockDim.x < nv; i += U * blockDim.x) {
+      uint4 t[U];
+#pragma unroll
+      for (uint32_t u = 0; u < U; ++u) t[u] = ld_stream(s4 + i + u * blockDim.x);
+#pragma unroll
+      for (uint32_t u = 0; u < U; ++u) d4[i + u * blockDim.x] = t[u];
+    }
+    for (; i < nv; i += blockDim.x) d4[i] = ld_stream(s4 + i);
+    for (uint32_t i = head + nv * VEC + threadIdx.x; i < len; i += blockDim.x) dst[off + i] = src[off + i];
+  };
   for (uint32_t c = blockIdx.x; c < nc; c += gridDim.x) {
     const CopyR r = rs[c];
-    for (uint32_t i = threadIdx.x; i < r.len; i += blockDim.x) {
-      Ak[r.offset + i] = Tk[r.offset + i];
-      if (VB) Av[r.offset + i] = Tv[r.offset + i];
-    }
+    col(Ak, Tk, r.offset, r.len);
+    if (VB) col(Av, Tv, r.offset, r.len);
   }
 }
 
