@@ -113,7 +113,7 @@ __device__ __forceinline__ T* opaque_ptr(T* p) {
 #if DTS_PHASE_PROF
 __device__ unsigned long long g_phase[16];
 // each kernel sets `ph_on` (DTS_PHASE_PROF == 1: scatter kernels, 2: local sort)
-#define PH_INIT unsigned long long ph_acc[10] = {0}; long long ph_t = clock64();
+#define PH_INIT unsigned long long ph_acc[11] = {0}; long long ph_t = clock64();
 #define PH(k)                                         \
   if (ph_on && tid == 0) {                            \
     const long long now_ = clock64();                 \
@@ -123,7 +123,7 @@ __device__ unsigned long long g_phase[16];
 #define PH_SPIN if (ph_on && tid < 512) atomicAdd(&g_phase[15], 1ull);
 #define PH_DONE                                                          \
   if (ph_on && tid == 0) {                                               \
-    for (int k_ = 0; k_ < 10; ++k_) atomicAdd(&g_phase[k_], ph_acc[k_]); \
+    for (int k_ = 0; k_ < 11; ++k_) atomicAdd(&g_phase[k_], ph_acc[k_]); \
     atomicAdd(&g_phase[14], 1ull);                                       \
   }
 #else

@@ -16,7 +16,7 @@ k = torch.empty_like(src); v = torch.empty_like(src)
 import os
 LOCAL = os.environ.get("DTS_PHASE", "1") == "2"
 if LOCAL:
-    names = ["tma wait", "keys+diff", "zero", "hist", "scan", "slots", "rank", "write-out", "-", "top"]
+    names = ["tma wait", "keys+diff", "zero(-)", "hist", "scan1", "scan2", "slots", "rank barrier", "write-out", "top", "rank (thread 0)"]
 elif os.environ.get("DTS_WC", "1") != "0":
     names = ["stripe/top", "tma wait", "rank", "pair scan", "binfo+map", "placement",
              "check+write-out", "-", "carry", "-"]
@@ -31,9 +31,9 @@ for rep in range(2):
     L.dts_debug_phases(buf, 16, 0)
 tiles = (r.kernel_records["local_sort"] / 4100.0) if LOCAL else (r.kernel_records["scatter"] / 4608.0)
 ctas = buf[14]
-tot = sum(buf[i] for i in range(10))
+tot = sum(buf[i] for i in range(11))
 print(f"tiles ~{tiles:.0f}  CTA-runs {ctas}  spins {buf[15]}  order-fixes wc {buf[13]} lookback {buf[12]}")
-for i, nm in enumerate(names):
+for i, nm in enumerate(names[:11]):
     print(f"{nm:16s} {buf[i]/tiles:9.0f} cycles/tile  {100*buf[i]/tot:5.1f}%")
 print(f"{'total':16s} {tot/tiles:9.0f} cycles/tile")
 if LOCAL and buf[12]:
