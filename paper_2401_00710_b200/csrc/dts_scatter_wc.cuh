@@ -20,6 +20,22 @@
 
 namespace dts {
 
+// (key, value) pair of one staging slot when both have the same width: one
+// 8/16-byte SMEM access per record instead of two (AoS staging)
+template <typename K> struct StPair;
+template <> struct StPair<uint32_t> {
+  using T = uint2;
+  __device__ static T make(uint32_t k, uint32_t v) { return make_uint2(k, v); }
+};
+template <> struct StPair<unsigned long> {
+  using T = ulonglong2;
+  __device__ static T make(unsigned long k, unsigned long v) { return make_ulonglong2(k, v); }
+};
+template <> struct StPair<unsigned long long> {
+  using T = ulonglong2;
+  __device__ static T make(unsigned long long k, unsigned long long v) { return make_ulonglong2(k, v); }
+};
+
 template <typename K, int VB> struct WcTile {
   static constexpr int NT = 512;  // (1024 threads measured slower: per-bucket phases)
   static constexpr int NW = NT / 32;
@@ -200,6 +216,27 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       PH(1)
       K* xk = bufk(cur);
       V* xv = bufv(cur);
+      // staging slot accessors (AoS pairs when key and value widths match;
+      // the pair array spans this tile's key+value buffer)
+      constexpr bool AOS = VB == (int)sizeof(K);
+      auto st_put = [&](uint32_t p, K k, V v) {
+        if constexpr (AOS) {
+          reinterpret_cast<typename StPair<K>::T*>(xk)[p] = StPair<K>::make(k, (K)v);
+        } else {
+          xk[p] = k;
+          if (VB) xv[p] = v;
+        }
+      };
+      auto st_get = [&](uint32_t p, K& k, V& v) {
+        if constexpr (AOS) {
+          const auto q = reinterpret_cast<const typename StPair<K>::T*>(xk)[p];
+          k = q.x;
+          v = (V)q.y;
+        } else {
+          k = xk[p];
+          if (VB) v = xv[p];
+        }
+      };
       const K* ik = xk + s_off[cur][0];
       const V* iv = xv + s_off[cur][1];
 
@@ -353,8 +390,7 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
         if (full || bk[i] != 0xFFFFu) {
           const uint32_t b = bk[i];
           const uint32_t p = ((mywh[b >> 1] >> ((b & 1u) << 4)) & 0xffffu) + lr[i];
-          xk[p] = key[i];
-          if (VB) xv[p] = val[i];
+          st_put(p, key[i], VB ? val[i] : V(0));
           pk[p] = (b << 16) | (warp * WS + i * 32 + lane);
         }
       }
@@ -378,8 +414,7 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
             kk = ck[D.w * CP + r];
             if (VB) vv = cv[D.w * CP + r];
           } else {
-            kk = xk[D.y + r];
-            if (VB) vv = xv[D.y + r];
+            st_get(D.y + r, kk, vv);
           }
           const uint32_t d = D.x + r;
           st_global(ko_seg + d, kk);
@@ -411,19 +446,20 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
             while (p + c < tn && ((pk[p + c] ^ x) < 65536u)) ++c;
             for (uint32_t a = 1; a < c; ++a) {
               const uint32_t xw = pk[p + a];
-              const K xk2 = xk[p + a];
+              K xk2;
               V xv2 = V(0);
-              if (VB) xv2 = xv[p + a];
+              st_get(p + a, xk2, xv2);
               uint32_t b2 = a;
               while (b2 > 0 && pk[p + b2 - 1] > xw) {
                 pk[p + b2] = pk[p + b2 - 1];
-                xk[p + b2] = xk[p + b2 - 1];
-                if (VB) xv[p + b2] = xv[p + b2 - 1];
+                K tk2;
+                V tv2 = V(0);
+                st_get(p + b2 - 1, tk2, tv2);
+                st_put(p + b2, tk2, tv2);
                 --b2;
               }
               pk[p + b2] = xw;
-              xk[p + b2] = xk2;
-              if (VB) xv[p + b2] = xv2;
+              st_put(p + b2, xk2, xv2);
             }
           }
         }
@@ -452,8 +488,7 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
           for (uint32_t u = 0; u < U; ++u) {
             if (i < (dw[u] >> 24)) {
               const uint32_t src = (dw[u] & 0xffffu) + i;
-              tk[u] = xk[src];
-              if (VB) tv[u] = xv[src];
+              st_get(src, tk[u], tv[u]);
             }
           }
 #pragma unroll
