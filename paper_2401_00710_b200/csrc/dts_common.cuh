@@ -97,22 +97,6 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // Lanes of the warp whose bucket equals this lane's (warp-level multisplit
 // peer set).  `nbits` ballots, one per bucket-id bit; deterministic cost and
 // no dependence on how many distinct ids the warp holds.
-__device__ __forceinline__ uint32_t peer_mask(uint32_t b, uint32_t valid_mask,
-                                              int nbits) {
-#ifdef DTS_USE_MATCH_ANY
-  (void)nbits;
-  return __match_any_sync(FULL, b) & valid_mask;
-#else
-  uint32_t m = valid_mask;
-  for (int i = 0; i < nbits; ++i) {
-    const uint32_t bit = (b >> i) & 1u;
-    const uint32_t bal = __ballot_sync(FULL, bit);
-    m &= bit ? bal : ~bal;
-  }
-  return m;
-#endif
-}
-
 // ---------------------------------------------------------------------------
 // Streaming loads / L2-sticky stores.  DTS_HINTS: 0 plain, 1 evict-first
 // loads, 2 evict-first loads + evict-last stores (keeps partially written
@@ -129,30 +113,6 @@ __device__ __forceinline__ T ld_stream(const T* p) {
   return *p;
 #endif
 }
-__device__ __forceinline__ uint64_t l2_policy_last() {
-  uint64_t pol = 0;
-#if DTS_HINTS >= 2
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-#endif
-  return pol;
-}
-__device__ __forceinline__ void st_keep(uint32_t* p, uint32_t v, uint64_t pol) {
-#if DTS_HINTS >= 2
-  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
-#else
-  (void)pol;
-  *p = v;
-#endif
-}
-__device__ __forceinline__ void st_keep(uint64_t* p, uint64_t v, uint64_t pol) {
-#if DTS_HINTS >= 2
-  asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
-#else
-  (void)pol;
-  *p = v;
-#endif
-}
-
 // ---------------------------------------------------------------------------
 // TMA 1-D bulk copies (cp.async.bulk) completed on an mbarrier.
 // ---------------------------------------------------------------------------
@@ -245,156 +205,6 @@ struct SplitRouter {
 
 // Block-wide exclusive scan of per-thread values (returns this thread's
 // exclusive prefix; *total receives the block total).  tmp: NT/32+1 words.
-template <int NT>
-__device__ __forceinline__ uint32_t block_exscan_val(uint32_t v, uint32_t* tmp, uint32_t* total) {
-  constexpr int NW = NT / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(FULL, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) tmp[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    const uint32_t w = lane < NW ? tmp[lane] : 0u;
-    uint32_t incl = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane < NW) tmp[lane] = incl - w;
-    if (lane == NW - 1) tmp[NW] = incl;
-  }
-  __syncthreads();
-  const uint32_t r = tmp[warp] + x - v;
-  *total = tmp[NW];
-  return r;
-}
-
-// Stable block radix rank with per-thread digit counters (counters laid
-// out [digit][thread] as u16, so a thread only touches its own column while
-// counting and the digit-major scan reproduces blocked input order).  Items
-// are in BLOCKED order: thread t owns positions t*IPT .. t*IPT+IPT-1.
-// `D` = number of digit values this pass (power of two, <= DMAX);
-// rank[i] receives the item's stable position in [0, NT*IPT).
-template <int NT, int IPT>
-__device__ __forceinline__ void block_rank(const uint32_t (&dig)[IPT], const int D,
-                                           uint32_t (&rank)[IPT], uint16_t* cnt,
-                                           uint32_t* tmp) {
-  const int t = threadIdx.x;
-  for (int d = 0; d < D; ++d) cnt[d * NT + t] = 0;
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    uint16_t* c = cnt + dig[i] * NT + t;
-    const uint32_t o = *c;
-    rank[i] = o;
-    *c = (uint16_t)(o + 1);
-  }
-  __syncthreads();
-  // raking exclusive scan over the D*NT counters in [digit][thread] order;
-  // thread t owns counters [t*D, t*D + D)
-  uint16_t* mine = cnt + t * D;
-  uint32_t sum = 0;
-  if (D >= 8) {
-    for (int k = 0; k < D; k += 8) {
-      const uint4 q = *reinterpret_cast<const uint4*>(mine + k);
-      sum += (q.x & 0xffffu) + (q.x >> 16) + (q.y & 0xffffu) + (q.y >> 16) + (q.z & 0xffffu) +
-             (q.z >> 16) + (q.w & 0xffffu) + (q.w >> 16);
-    }
-  } else {
-    for (int k = 0; k < D; ++k) sum += mine[k];
-  }
-  uint32_t total;
-  uint32_t run = block_exscan_val<NT>(sum, tmp, &total);
-  if (D >= 8) {
-    for (int k = 0; k < D; k += 8) {
-      uint4 q = *reinterpret_cast<const uint4*>(mine + k);
-      uint32_t* w = reinterpret_cast<uint32_t*>(&q);
-#pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const uint32_t lo = w[h] & 0xffffu, hi = w[h] >> 16;
-        const uint32_t a = run, b = run + lo;
-        run = b + hi;
-        w[h] = (a & 0xffffu) | (b << 16);
-      }
-      *reinterpret_cast<uint4*>(mine + k) = q;
-    }
-  } else {
-    for (int k = 0; k < D; ++k) {
-      const uint32_t v = mine[k];
-      mine[k] = (uint16_t)run;
-      run += v;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) rank[i] += cnt[dig[i] * NT + t];
-}
-
-// Packed variant (CUB-style): u32 counter words laid out [lane][thread],
-// lane = d mod H (H = D/2), each word packing the u16 counts of digits
-// `lane` (low half) and `lane + H` (high half).  The digit-major scan then
-// runs on packed words (both halves at once), and high-half digits add the
-// low-half grand total.  `addr` caches each item's counter word index.
-template <int NT, int IPT>
-__device__ __forceinline__ void block_rank_packed(const uint32_t (&dig)[IPT], const int hbits,
-                                                  uint32_t (&rank)[IPT], uint32_t* cnt,
-                                                  uint32_t* tmp) {
-  const int t = threadIdx.x;
-  const int H = 1 << hbits;  // D = 2H digit values
-  uint32_t* col = cnt + t;
-  for (int l = 0; l < H; ++l) col[l * NT] = 0u;
-  uint32_t widx[IPT];
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const uint32_t d = dig[i];
-    const uint32_t sh = (d >> hbits) << 4;
-    widx[i] = (d & (uint32_t)(H - 1)) * NT;
-    const uint32_t w = col[widx[i]];
-    rank[i] = (w >> sh) & 0xffffu;
-    col[widx[i]] = w + (1u << sh);
-  }
-  __syncthreads();
-  // raking scan: thread t owns packed words [t*H, t*H + H) of the [lane][thread] array
-  uint32_t* mine = cnt + t * H;
-  uint32_t sum = 0;
-  if (H >= 4) {
-    for (int k = 0; k < H; k += 4) {
-      const uint4 q = *reinterpret_cast<const uint4*>(mine + k);
-      sum += q.x + q.y + q.z + q.w;
-    }
-  } else {
-    for (int k = 0; k < H; ++k) sum += mine[k];
-  }
-  uint32_t total;
-  uint32_t run = block_exscan_val<NT>(sum, tmp, &total);
-  if (H >= 4) {
-    for (int k = 0; k < H; k += 4) {
-      uint4 q = *reinterpret_cast<const uint4*>(mine + k);
-      const uint32_t a = run, b = a + q.x, c = b + q.y, e = c + q.z;
-      run = e + q.w;
-      *reinterpret_cast<uint4*>(mine + k) = make_uint4(a, b, c, e);
-    }
-  } else {
-    for (int k = 0; k < H; ++k) {
-      const uint32_t v = mine[k];
-      mine[k] = run;
-      run += v;
-    }
-  }
-  __syncthreads();
-  const uint32_t lo_total = total & 0xffffu;
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const uint32_t hi = dig[i] >> hbits;
-    const uint32_t w = col[widx[i]];
-    rank[i] += ((w >> (hi << 4)) & 0xffffu) + (hi ? lo_total : 0u);
-  }
-}
-
 // Block-wide exclusive scan of a[0..n) in shared memory (in place); returns
 // the total.  All threads of the block must call it.  `tmp` holds NT/32
 // entries.

@@ -102,11 +102,6 @@ __device__ __forceinline__ T* opaque_ptr(T* p) {
 
 // DTS_PHASE_PROF=1 (tools build only): thread 0 of every CTA accumulates
 // clock64() cycles per tile phase; read back with dts_debug_phases().
-// DTS_SCATTER_EXP (experiment builds only, results are WRONG): bit 0 drops
-// the global stores of the write-out, bit 1 drops the look-back waits.
-#ifndef DTS_SCATTER_EXP
-#define DTS_SCATTER_EXP 0
-#endif
 #ifndef DTS_PHASE_PROF
 #define DTS_PHASE_PROF 0
 #endif
@@ -405,7 +400,7 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
       uint32_t ex = 0;
 #pragma unroll
       for (int j = 0; j < LB - 1; ++j) {
-        if ((uint32_t)j < kt && !(DTS_SCATTER_EXP & 2)) {
+        if ((uint32_t)j < kt) {
           while (!(v[j] & ST_VALID)) {
             PH_SPIN
             __nanosleep(64);
@@ -440,12 +435,8 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
         bad |= ((wd ^ nx) < 65536u) & (nx < wd);
         const uint32_t e = wd & 0xffffu;
         const uint32_t d = db[wd >> 16] + p;
-        if (DTS_SCATTER_EXP & 1) {
-          bad |= ((uint32_t)sk[e] ^ (uint32_t)sv[e] ^ d) == 0x12345u;
-        } else {
-          st_global(ko_seg + d, sk[e]);
-          if (VB) st_global(vo_seg + d, sv[e]);
-        }
+        st_global(ko_seg + d, sk[e]);
+        if (VB) st_global(vo_seg + d, sv[e]);
       }
     } else {
 #pragma unroll

@@ -1,8 +1,6 @@
-// dts_sort_kernels.cuh — the distribution and base-case kernels:
-//   k_histogram  : per-block bucket counts            (counting.py:123-137)
-//   k_scatter    : stable tile-ranked scatter          (counting.py:141-151,
-//                                                       _kernels.py:12-25)
-//   k_local_sort : SMEM stable LSD sort of spans       (dtsort.py:127-147)
+// dts_sort_kernels.cuh — k_histogram, the per-block bucket counts of a
+// distribution pass (counting.py:123-137).  The scatters are in
+// dts_scatter.cuh / dts_scatter_wc.cuh, the base case in dts_local.cuh.
 #pragma once
 #include "dts_kernels.cuh"
 
@@ -84,45 +82,6 @@ __global__ void __launch_bounds__(NT) k_histogram(const SegPlan* __restrict__ pl
     for (uint32_t b = tid; b < P.nbmax; b += NT) row[(uint64_t)b * P.nrows] = hist[b];
     __syncthreads();
   }
-}
-
-// ---------------------------------------------------------------------------
-// Tile staging: copy [g0, g0+tn) of a global column into SMEM so that element
-// e lands at buf[off + e] with off = g0 % (16/sizeof(T)); the 16-byte aligned
-// body moves as uint4 (LDG.128/STS.128), head/tail elementwise.
-// ---------------------------------------------------------------------------
-template <typename T, int NT>
-__device__ __forceinline__ uint32_t stage_tile(T* buf, const T* __restrict__ src, uint64_t g0,
-                                               uint32_t tn) {
-  constexpr int VEC = 16 / sizeof(T);
-  const uint32_t off = (uint32_t)(g0 % VEC);
-  T* dst = buf + off;
-  const T* s = src + g0;
-  // elements before the first aligned one
-  const uint32_t head0 = (VEC - off) % VEC;
-  const uint32_t head = head0 < tn ? head0 : tn;
-  const uint32_t nvec = (tn - head) / VEC;
-  const uint32_t tail0 = head + nvec * VEC;
-  const int tid = threadIdx.x;
-  if ((uint32_t)tid < head) dst[tid] = ld_stream(s + tid);
-  if ((uint32_t)tid < tn - tail0) dst[tail0 + tid] = ld_stream(s + tail0 + tid);
-  const uint4* sv = reinterpret_cast<const uint4*>(s + head);
-  uint4* dv = reinterpret_cast<uint4*>(dst + head);
-  constexpr int U = 8;
-  for (uint32_t b = 0; b < nvec; b += NT * U) {
-    uint4 r[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t i = b + u * NT + tid;
-      if (i < nvec) r[u] = ld_stream(sv + i);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t i = b + u * NT + tid;
-      if (i < nvec) dv[i] = r[u];
-    }
-  }
-  return off;
 }
 
 }  // namespace dts
