@@ -225,7 +225,7 @@ def run_ours(args, cfgd, rank, world, local_rank):
     from paper_2401_00710_b200 import _lib
 
     ws = torch.empty(int(_lib.lib().dts_workspace_bytes(n, kb, vb)), dtype=torch.uint8, device=dev)
-    multi = world > 1
+    multi = world > 1 or args.force_dist
     if multi:
         from paper_2401_00710_b200.distributed import CudaOps, dist_sort
 
@@ -357,6 +357,46 @@ def run_ours(args, cfgd, rank, world, local_rank):
                "h2d_bytes_per_step": n * (kb + vb), "d2h_bytes_per_step": n * (kb + vb),
                "ms_per_step": round(e_ms, 2), "steps": e_steps,
                "path": "dt_sort(RecordArray(pinned host tensors)) -> H2D, dts_sort, D2H"}
+    elif multi and not args.no_e2e:
+        # every rank: pinned host slice -> device, dist_sort, result -> pinned
+        # host; max over ranks of the wall time between barriers
+        hk = src_k.cpu().pin_memory()
+        hv = None if src_v is None else src_v.cpu().pin_memory()
+        cap = n + n // 2  # pinned result buffers (ranks receive ~n records)
+        ok_b = torch.empty(cap, dtype=src_k.dtype, pin_memory=True)
+        ov_b = None if src_v is None else torch.empty(cap, dtype=src_v.dtype, pin_memory=True)
+        e_steps = max(1, min(args.steps, args.e2e_steps))
+        e_ms = 0.0
+        out_bytes = 0
+        for i in range(e_steps + 1):
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            dk = hk.to(dev, non_blocking=True)
+            dv = None if hv is None else hv.to(dev, non_blocking=True)
+            rk, rv, st = dist_sort(dk, dv, ops=ops)
+            m = rk.numel()
+            if m > ok_b.numel():
+                ok_b = torch.empty(m, dtype=rk.dtype, pin_memory=True)
+                if ov_b is not None:
+                    ov_b = torch.empty(m, dtype=rv.dtype, pin_memory=True)
+            ok_h = ok_b[:m]
+            ok_h.copy_(rk, non_blocking=True)
+            ov_h = None
+            if rv is not None:
+                ov_h = ov_b[:m]
+                ov_h.copy_(rv, non_blocking=True)
+            torch.cuda.synchronize()
+            t = torch.tensor([(time.perf_counter() - t0) * 1e3], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            if i > 0:
+                e_ms += float(t.item())
+            out_bytes = ok_h.numel() * ok_h.element_size() + (0 if ov_h is None else ov_h.numel() * ov_h.element_size())
+        e_ms /= e_steps
+        e2e = {"value": round(n * world / (e_ms / 1e3) / 1e9, 4), "unit": UNIT,
+               "h2d_bytes_per_step": n * (kb + vb), "d2h_bytes_per_step": int(out_bytes),
+               "ms_per_step": round(e_ms, 2), "steps": e_steps, "per_rank": True,
+               "path": "per rank: pinned host slice -> H2D, distributed.dist_sort (NCCL all-to-all), D2H"}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -396,6 +436,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the multi-GPU path (dist_sort) even at world size 1 (testing)")
     args = ap.parse_args()
     cfgd = dict(CONFIGS[args.config])
     if args.n:
@@ -406,7 +448,8 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfgd, rank, world)
         return
-    if world > 1:
+    use_dist = world > 1 or args.force_dist
+    if use_dist:
         import torch
         import torch.distributed as dist
 
@@ -415,7 +458,7 @@ def main():
     try:
         run_ours(args, cfgd, rank, world, local_rank)
     finally:
-        if world > 1:
+        if use_dist:
             import torch.distributed as dist
 
             dist.destroy_process_group()
