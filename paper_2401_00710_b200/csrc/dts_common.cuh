@@ -187,13 +187,42 @@ struct Router {
 
 // Partition router: destination = number of (key, index) splitters strictly
 // below the record (SURVEY.md §8e composite splitters).
+// Lanes of the warp holding the same small id b (< 2^nbits) as this lane,
+// from nbits ballots (`valid` lanes only).
+__device__ __forceinline__ uint32_t warp_peers(uint32_t b, bool valid, int nbits) {
+  uint32_t m = __ballot_sync(FULL, valid);
+  for (int i = 0; i < nbits; ++i) {
+    const bool bit = (b >> i) & 1u;
+    const uint32_t bb = __ballot_sync(FULL, bit);
+    m &= bit ? bb : ~bb;
+  }
+  return m;
+}
+
+// Destination rank of a record: the number of (key, global index) splitters
+// strictly below it.  With <= 15 splitters a 1024-entry prefix table (top 10
+// key bits -> first splitter of the prefix | splitters in it << 4) answers
+// most keys with one SMEM load; keys sharing a prefix with a splitter compare
+// against those few.
+constexpr int SPLIT_TB = 10;
 template <typename K>
 struct SplitRouter {
   const K* sk;
   const uint64_t* si;
   uint32_t ns;
+  const uint8_t* tab;  // nullptr: binary search
   __device__ __forceinline__ uint32_t operator()(K key, uint64_t gidx) const {
-    uint32_t lo = 0, hi = ns;
+    uint32_t lo, hi;
+    if (tab) {
+      const uint32_t e = tab[(uint32_t)(key >> (sizeof(K) * 8 - SPLIT_TB))];
+      lo = e & 15u;
+      const uint32_t c = e >> 4;
+      if (c == 0) return lo;
+      hi = lo + c;
+    } else {
+      lo = 0;
+      hi = ns;
+    }
     while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;
       const bool less = sk[mid] < key || (sk[mid] == key && si[mid] < gidx);
@@ -203,8 +232,6 @@ struct SplitRouter {
   }
 };
 
-// Block-wide exclusive scan of per-thread values (returns this thread's
-// exclusive prefix; *total receives the block total).  tmp: NT/32+1 words.
 // Block-wide exclusive scan of a[0..n) in shared memory (in place); returns
 // the total.  All threads of the block must call it.  `tmp` holds NT/32
 // entries.

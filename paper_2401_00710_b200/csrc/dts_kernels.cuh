@@ -31,7 +31,7 @@ __host__ __device__ inline HistLayout hist_layout(int kb, Caps c, bool split) {
   L.hk = o; o = align16(o + (size_t)c.hkc * kb);
   L.si = o; o = align16(o + (split ? (size_t)c.hkc * 8 : 0));
   L.hist = o; o = align16(o + (size_t)c.nbc * 4);
-  L.hz = o; o = align16(o + (size_t)c.hzc * 4);
+  L.hz = o; o = align16(o + (size_t)(split ? (c.hzc > 256 ? c.hzc : 256) : c.hzc) * 4);  // split: prefix table
   L.total = o;
   return L;
 }
@@ -47,6 +47,20 @@ __device__ __forceinline__ void load_tables(const SegPlan& P, const K* __restric
     for (uint32_t i = threadIdx.x; i < P.nheavy; i += blockDim.x) {
       hk[i] = heavy_pool[P.heavy_base + i];
       si[i] = split_idx[P.heavy_base + i];
+    }
+    if (P.nheavy <= 15) {  // prefix table (SplitRouter), in the hz area
+      __syncthreads();       // (block-uniform call) splitter keys are in hk
+      uint8_t* tab = reinterpret_cast<uint8_t*>(hz);
+      constexpr int W = sizeof(K) * 8;
+      for (uint32_t pfx = threadIdx.x; pfx < (1u << SPLIT_TB); pfx += blockDim.x) {
+        uint32_t below = 0, in = 0;
+        for (uint32_t j = 0; j < P.nheavy; ++j) {
+          const uint32_t sp = (uint32_t)(hk[j] >> (W - SPLIT_TB));
+          below += sp < pfx;
+          in += sp == pfx;
+        }
+        tab[pfx] = (uint8_t)(below | (in << 4));
+      }
     }
   } else if (P.flags & PF_HEAVY) {
     const uint32_t nz = (1u << P.gamma) + 1u;

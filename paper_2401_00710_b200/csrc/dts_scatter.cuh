@@ -40,7 +40,7 @@ template <typename K, int VB, bool SPLIT> struct ScatterSmem {
   static constexpr size_t hk = a16(db + (size_t)TL::NBC * 4);
   static constexpr size_t si = a16(hk + (size_t)(SPLIT ? TL::HKC : 256) * sizeof(K));
   static constexpr size_t hz = a16(si + (SPLIT ? (size_t)TL::HKC * 8 : 0));
-  static constexpr size_t geo = a16(hz + (SPLIT ? 0 : (size_t)TL::HZC * 4));
+  static constexpr size_t geo = a16(hz + (SPLIT ? ((size_t)1 << SPLIT_TB) : (size_t)TL::HZC * 4));
   static constexpr size_t plan = a16(geo + 2 * 32);
   static constexpr size_t bar = a16(plan + 2 * sizeof(SegPlan));
   static constexpr size_t total = a16(bar + 16);
@@ -295,18 +295,37 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
         rank_one(i, key >= thr ? ovfb : ((uint32_t)(key >> shift) & mask));
         __syncwarp();
       }
-    } else {
-      const Router<K> R = make_router<K>(P, hz, hk);
+    } else if (SPLIT) {
+      // few destinations (G ranks): ranks from ballot peer masks; the first
+      // lane of each group bumps the warp's u16 counter (no atomics, so no
+      // same-address serialisation and no reliance on atomic order)
       SplitRouter<K> SR;
       SR.sk = hk; SR.si = si; SR.ns = P.nheavy;
+      SR.tab = P.nheavy <= 15 ? reinterpret_cast<const uint8_t*>(hz) : nullptr;
+      uint16_t* myc16 = reinterpret_cast<uint16_t*>(mywh);
+      const int nbits = nb > 1 ? 32 - __clz((int)(nb - 1)) : 0;
+#pragma unroll
+      for (int i = 0; i < IPT; ++i) {
+        const uint32_t e = warp * WS + i * 32 + lane;
+        const bool valid = e < tn;
+        const uint32_t b = valid ? SR(sk[e], global_base + g0 + e) : 0u;
+        const uint32_t peers = warp_peers(b, valid, nbits);
+        const uint32_t before = __popc(peers & lanemask_lt());
+        uint32_t base = 0;
+        if (valid) base = myc16[b];
+        __syncwarp();
+        bk[i] = valid ? b : 0xFFFFu;
+        lr[i] = base + before;
+        if (valid && before == 0) myc16[b] = (uint16_t)(base + __popc(peers));
+        __syncwarp();
+      }
+    } else {
+      const Router<K> R = make_router<K>(P, hz, hk);
 #pragma unroll
       for (int i = 0; i < IPT; ++i) {
         const uint32_t e = warp * WS + i * 32 + lane;
         bk[i] = 0xFFFFu;
-        if (e < tn) {
-          const K key = sk[e];
-          rank_one(i, SPLIT ? SR(key, global_base + g0 + e) : R(key));
-        }
+        if (e < tn) rank_one(i, R(sk[e]));
         __syncwarp();
       }
     }

@@ -46,19 +46,34 @@ __global__ void __launch_bounds__(NT) k_histogram(const SegPlan* __restrict__ pl
     const Router<K> R = make_router<K>(P, hz, hk);
     SplitRouter<K> SR;
     SR.sk = hk; SR.si = si; SR.ns = P.nheavy;
+    SR.tab = (SPLIT && P.nheavy <= 15) ? reinterpret_cast<const uint8_t*>(hz) : nullptr;
     const K* p = keys + B.begin;
     const uint64_t n = B.end - B.begin;
     auto count_one = [&](K key, uint64_t e) {
       const uint32_t b = SPLIT ? SR(key, global_base + B.begin + e) : R(key);
       atomicAdd(&hist[b], 1u);
     };
+    // partition (<= 8 destinations): 8-bit counters packed in one u64
+    // register per thread (a thread counts < 256 keys of a block), reduced
+    // over the warp at the end of the block
+    const bool packed = SPLIT && P.nb <= 8;
+    unsigned long long pc = 0ull;
+    auto count_split = [&](K key, uint64_t e) {
+      const uint32_t b = SR(key, global_base + B.begin + e);
+      if (packed) pc += 1ull << (8 * b);
+      else atomicAdd(&hist[b], 1u);
+    };
     const uint64_t addr = reinterpret_cast<uint64_t>(p);
     uint64_t head = ((16 - (addr & 15)) & 15) / sizeof(K);
     if (head > n) head = n;
     const uint64_t nvec = (n - head) / VEC;
     const uint64_t tail0 = head + nvec * VEC;
-    if ((uint64_t)tid < head) count_one(p[tid], tid);
-    if ((uint64_t)tid < n - tail0) count_one(p[tail0 + tid], tail0 + tid);
+    if ((uint64_t)tid < head) {
+      if (SPLIT) count_split(p[tid], tid); else count_one(p[tid], tid);
+    }
+    if ((uint64_t)tid < n - tail0) {
+      if (SPLIT) count_split(p[tail0 + tid], tail0 + tid); else count_one(p[tail0 + tid], tail0 + tid);
+    }
     const uint4* pv = reinterpret_cast<const uint4*>(p + head);
     for (uint64_t vb = 0; vb < nvec; vb += (uint64_t)NT * U) {
       uint4 v[U];
@@ -70,11 +85,26 @@ __global__ void __launch_bounds__(NT) k_histogram(const SegPlan* __restrict__ pl
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint64_t vi = vb + (uint64_t)u * NT + tid;
-        if (vi < nvec) {
+        if (SPLIT) {
+          if (vi < nvec) {
+            const K* kk = reinterpret_cast<const K*>(&v[u]);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) count_split(kk[e], head + vi * VEC + e);
+          }
+        } else if (vi < nvec) {
           const K* kk = reinterpret_cast<const K*>(&v[u]);
 #pragma unroll
           for (int e = 0; e < VEC; ++e) count_one(kk[e], head + vi * VEC + e);
         }
+      }
+    }
+    if (SPLIT && packed) {
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        uint32_t c = (uint32_t)(pc >> (8 * b)) & 0xffu;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+        if ((threadIdx.x & 31) == 0 && c) atomicAdd(&hist[b], c);
       }
     }
     __syncthreads();

@@ -85,8 +85,10 @@ class CudaOps:
         ov = None if vals is None else torch.empty_like(vals)
         counts = np.zeros(G, np.uint64)
         L = _lib.lib()
-        ws = torch.empty(int(L.dts_workspace_bytes(n, kb, vb)), dtype=torch.uint8,
-                         device=keys.device)
+        # the partition uses the workspace for its metadata only (count
+        # matrix, scan, tile lists): far less than a sort workspace
+        need = min(int(L.dts_workspace_bytes(n, kb, vb)), (32 << 20) + n * (G + 4) // 512)
+        ws = torch.empty(need, dtype=torch.uint8, device=keys.device)
         skc = np.ascontiguousarray(split_keys.astype(np.uint32 if kb == 4 else np.uint64))
         sic = np.ascontiguousarray(split_idx.astype(np.uint64))
         stream = torch.cuda.current_stream(keys.device).cuda_stream
