@@ -60,6 +60,7 @@ class CudaOps:
     def __init__(self, cfg: SortConfig | None = None, mode: int = _lib.MODE_DT):
         self.cfg = cfg or SortConfig()
         self.mode = mode
+        self._ws = None  # partition workspace, reused across calls
 
     def sample(self, keys, gbase: int, count: int, seed: int):
         import torch
@@ -88,7 +89,9 @@ class CudaOps:
         # the partition uses the workspace for its metadata only (count
         # matrix, scan, tile lists): far less than a sort workspace
         need = min(int(L.dts_workspace_bytes(n, kb, vb)), (32 << 20) + n * (G + 4) // 512)
-        ws = torch.empty(need, dtype=torch.uint8, device=keys.device)
+        ws = self._ws
+        if ws is None or ws.numel() < need or ws.device != keys.device:
+            ws = self._ws = torch.empty(need, dtype=torch.uint8, device=keys.device)
         skc = np.ascontiguousarray(split_keys.astype(np.uint32 if kb == 4 else np.uint64))
         sic = np.ascontiguousarray(split_idx.astype(np.uint64))
         stream = torch.cuda.current_stream(keys.device).cuda_stream
