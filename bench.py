@@ -261,6 +261,8 @@ def run_ours(args, cfgd, rank, world, local_rank):
     total_ms = 0.0
     reps = []
     stream = torch.cuda.current_stream(dev)
+    if multi:
+        ops.launches = 0
     for _ in range(args.steps):
         restore()
         torch.cuda.synchronize()
@@ -292,7 +294,7 @@ def run_ours(args, cfgd, rank, world, local_rank):
     # library on the launching stream, summed over the timed steps
     peak, peak_kind = peaks()
     roof = None
-    launches = None
+    launches = int(ops.launches) if multi else None
     if not multi and reps and reps[0] is not None:
         sc_ms = sum(r.kernel_ms["scatter"] for r in reps)
         sc_launch = sum(r.kernel_launches["scatter"] for r in reps)

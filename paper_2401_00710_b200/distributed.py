@@ -61,6 +61,7 @@ class CudaOps:
         self.cfg = cfg or SortConfig()
         self.mode = mode
         self._ws = None  # partition workspace, reused across calls
+        self.launches = 0  # libdts kernels launched (partition + local sort)
 
     def sample(self, keys, gbase: int, count: int, seed: int):
         import torch
@@ -108,12 +109,15 @@ class CudaOps:
             kb, vb, ctypes.c_void_p(ws.data_ptr()), int(ws.numel()), ctypes.c_void_p(stream),
         )
         _lib.check(rc)
+        self.launches += 6  # histogram, 3 scan kernels, bounds, scatter
         return ok, ov, [int(c) for c in counts]
 
     def sort(self, keys, vals):
         from .dtsort import sort_device
 
-        return sort_device(keys, vals, self.cfg, self.mode, report=True)
+        rep = sort_device(keys, vals, self.cfg, self.mode, report=True)
+        self.launches += int(rep.gpu_launches)
+        return rep
 
     def empty_like(self, t, n):
         import torch
