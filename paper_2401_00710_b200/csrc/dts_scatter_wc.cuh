@@ -37,9 +37,11 @@ template <> struct StPair<unsigned long long> {
 };
 
 template <typename K, int VB> struct WcTile {
-  static constexpr int NT = 512;  // (1024 threads measured slower: per-bucket phases)
+  // 512 threads: 768 (16.4 ms) and 1024 measured slower on C2 — the
+  // per-bucket phases lengthen with the warp count
+  static constexpr int NT = 512;
   static constexpr int NW = NT / 32;
-  static constexpr int PT = NT / 512;  // threads per bucket pair in the pair phases
+  static constexpr int PT = 1;  // threads per bucket pair in the pair phases
   static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? 9 : 5;
   static constexpr int WS = 32 * IPT;
   static constexpr int T = NT * IPT;
@@ -243,12 +245,11 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       // ---- route + per-warp rank; records into registers ----
       K key[IPT];
       V val[IPT];
-      uint32_t bk[IPT], lr[IPT];
+      uint32_t bk[IPT];  // bucket << 16 | rank within the warp's bucket run
       auto rank_one = [&](int i, uint32_t b) {
         const uint32_t sh = (b & 1u) << 4;
         const uint32_t old = atomicAdd(&mywh[b >> 1], 1u << sh);
-        bk[i] = b;
-        lr[i] = (old >> sh) & 0xffffu;
+        bk[i] = (b << 16) | ((old >> sh) & 0xffffu);
       };
       if (full && !(P.flags & PF_HEAVY)) {
         const uint32_t shift = P.shift, mask = (1u << P.gamma) - 1u;
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
           const uint32_t e = warp * WS + i * 32 + lane;
-          bk[i] = 0xFFFFu;
+          bk[i] = 0xFFFFFFFFu;
           if (e < tn) {
             key[i] = ik[e];
             if (VB) val[i] = iv[e];
@@ -387,9 +388,9 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       // ---- placement into the staging area (this tile's buffer) ----
 #pragma unroll
       for (int i = 0; i < IPT; ++i) {
-        if (full || bk[i] != 0xFFFFu) {
-          const uint32_t b = bk[i];
-          const uint32_t p = ((mywh[b >> 1] >> ((b & 1u) << 4)) & 0xffffu) + lr[i];
+        if (full || bk[i] != 0xFFFFFFFFu) {
+          const uint32_t b = bk[i] >> 16;
+          const uint32_t p = ((mywh[b >> 1] >> ((b & 1u) << 4)) & 0xffffu) + (bk[i] & 0xffffu);
           st_put(p, key[i], VB ? val[i] : V(0));
           pk[p] = (b << 16) | (warp * WS + i * 32 + lane);
         }
