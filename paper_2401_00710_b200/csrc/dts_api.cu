@@ -285,11 +285,14 @@ struct Sorter {
 
   Sorter(Timer& t) : tm(t) {}
 
+  // Digit width of a segment: just enough buckets for children of ~thr/2
+  // records (the reference's γ_lo floor, core.py:156-164, is not applied:
+  // small segments split into few, large buckets — fewer, longer runs;
+  // the output does not depend on γ).
   uint32_t choose_gamma(uint64_t len, uint32_t remaining) const {
     const uint64_t target = std::max<uint64_t>(1, thr / 2);
     uint32_t need = ceil_log2_u64((len + target - 1) / target);
-    uint32_t g = std::max(need, std::min(glo, gcap));
-    g = std::min(g, gcap);
+    uint32_t g = std::min(need, gcap);
     g = std::min(g, remaining);
     return std::max<uint32_t>(g, 1);
   }
@@ -297,9 +300,11 @@ struct Sorter {
   // dt_sort sampling decision (dtsort.py:225-228: sample only when the
   // segment holds at least SAMPLE_FACTOR x the sample).  Adjusts g (<= 9)
   // and returns the subsample exponent gs (|S| = 2^gs * stride).
-  bool sampled_plan(uint64_t len, uint32_t remaining, uint32_t& g, uint32_t& gs) const {
+  // Below the root the strided subsample has <= 2^7 entries (heavy keys of
+  // >= 1/128 of a segment): each sampled segment sorts its sample in one CTA.
+  bool sampled_plan(uint64_t len, uint32_t remaining, uint32_t& g, uint32_t& gs, bool root) const {
     const uint32_t g9 = std::min<uint32_t>(g, gcap_hw > 1 ? gcap_hw - 1 : 1);
-    gs = std::min<uint32_t>(g9 > 1 ? g9 - 1 : 1, gs_max);
+    gs = std::min<uint32_t>(g9 > 1 ? g9 - 1 : 1, root ? gs_max : std::min<uint32_t>(gs_max, 7));
     uint64_t S = std::min<uint64_t>(len, (uint64_t(1) << gs) * stride);
     S = std::min<uint64_t>(S, smax);
     if (len < SAMPLE_FACTOR * S) return false;
@@ -420,7 +425,7 @@ struct Sorter {
       P.nb = 1u << g;
       P.nbmax = P.nb;
       uint32_t gs = 0;
-      if (dt && sampled_plan(hs.len, remaining, g, gs)) {
+      if (dt && sampled_plan(hs.len, remaining, g, gs, hs.root && hs.consumed == 0)) {
         // sampled segments may gain heavy / overflow buckets; the digit is
         // capped so bucket ids stay below the scatter's 2^10 capacity
         P.gamma = g;
