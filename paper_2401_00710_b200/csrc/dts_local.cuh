@@ -6,14 +6,17 @@
 namespace dts {
 
 template <typename K, int VB> struct LocalTile {
-  static constexpr int NT = 512;
+  // 8 warps: one 4-bit per-warp field per bin in a 32-bit bin word (the
+  // stable counting path below); 2 CTAs per SM
+  static constexpr int NT = 256;
   static constexpr int NW = NT / 32;
-  static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? 9 : 5;
+  static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? 18 : 10;
   static constexpr int WS = 32 * IPT;  // records per warp sub-tile
   static constexpr int CAP = NT * IPT; // records per span
   static constexpr int RB = 8;         // LSD radix bits per pass (fallback path)
-  static constexpr int CB = 13;        // counting path: spans differing in <= CB bits
-  static constexpr int FIXMAX = 64;    // counting path: largest equal-key group
+  static constexpr int NB = 12;        // nibble counting path: spans differing in <= NB bits
+  static constexpr int CB = 13;        // packed counting path: top CB differing bits
+  static constexpr int FIXMAX = 64;    // packed counting path: largest equal-key group
 };
 
 // Compile-time SMEM layout: two span buffers (TMA double buffering), the
@@ -177,33 +180,19 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
     }
 
     bool lsd = false;
-    {
-      // ================= counting path: one pass on the top <= CB differing
-      // bits; records sharing those bits are ranked by (key, position) ======
-      const int dbits = bits < TL::CB ? bits : TL::CB;
-      const int dsh = bits - dbits;  // bits below the digit (0: digit = whole order)
-      const uint32_t nbin = 1u << dbits, mask = nbin - 1u, nwd = (nbin + 1) >> 1;
-      // (the bins are zero here: zeroed at start and after every span)
-      PH(2)
-#pragma unroll
-      for (int i = 0; i < IPT; ++i) {
-        const uint32_t e = warp * WS + i * 32 + lane;
-        if (e < n) {
-          const uint32_t d = (uint32_t)(key[i] >> dsh) & mask;
-          atomicAdd(&cnt[d >> 1], 1u << ((d & 1u) << 4));
-        }
-      }
-      __syncthreads();
-      PH(3)
-      // exclusive scan over the bins (thread-contiguous word ranges), and the
-      // largest group
-      const uint32_t wpt = (nwd + NT - 1) / NT;
-      const uint32_t w0 = min(nwd, tid * wpt), w1 = min(nwd, w0 + wpt);
+    // exclusive scan over packed u16 bin pairs cnt[0..nwd) (uint4 quads, a
+    // contiguous range per thread); sets s_big when a bin exceeds FIXMAX
+    auto scan_bins = [&](uint32_t nwd) {
+      const uint32_t nq = (nwd + 3) >> 2, qpt = (nq + NT - 1) / NT;
+      const uint32_t q0 = min(nq, tid * qpt), q1 = min(nq, q0 + qpt);
+      uint4* cq = reinterpret_cast<uint4*>(cnt);
       uint32_t sum = 0, mx = 0;
-      for (uint32_t w = w0; w < w1; ++w) {
-        const uint32_t x = cnt[w];
-        sum += (x & 0xffffu) + (x >> 16);
-        mx = max(mx, max(x & 0xffffu, x >> 16));
+      for (uint32_t q = q0; q < q1; ++q) {
+        const uint4 x = cq[q];
+        sum += (x.x & 0xffffu) + (x.x >> 16) + (x.y & 0xffffu) + (x.y >> 16) + (x.z & 0xffffu) +
+               (x.z >> 16) + (x.w & 0xffffu) + (x.w >> 16);
+        const uint32_t m2 = __vmaxu2(__vmaxu2(x.x, x.y), __vmaxu2(x.z, x.w));
+        mx = max(mx, max(m2 & 0xffffu, m2 >> 16));
       }
       uint32_t incl = sum;
 #pragma unroll
@@ -225,17 +214,185 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
       }
       const uint32_t wex = __shfl_sync(FULL, wp, (warp + 31) & 31);
       uint32_t base = (warp ? wex : 0u) + incl - sum;
-      for (uint32_t w = w0; w < w1; ++w) {
-        const uint32_t x = cnt[w];
-        const uint32_t lo = x & 0xffffu;
-        cnt[w] = base | ((base + lo) << 16);
+      auto ex = [&](uint32_t x) {
+        const uint32_t lo = x & 0xffffu, r = base | ((base + lo) << 16);
         base += lo + (x >> 16);
+        return r;
+      };
+      for (uint32_t q = q0; q < q1; ++q) {
+        uint4 x = cq[q];
+        x.x = ex(x.x);
+        x.y = ex(x.y);
+        x.z = ex(x.z);
+        x.w = ex(x.w);
+        cq[q] = x;
       }
       __syncthreads();
+    };
+    auto zero_bins = [&](uint32_t nwd) {
+      const uint32_t nq = (nwd + 3) >> 2;
+      for (uint32_t q = tid; q < nq; q += NT) reinterpret_cast<uint4*>(cnt)[q] = make_uint4(0u, 0u, 0u, 0u);
+    };
+    if (bits <= TL::NB) {
+      // ================= nibble counting path: the differing bits are the
+      // whole key order, so ONE stable counting pass sorts the span.  Bin
+      // word d holds a 4-bit count per warp (warp w at bits 4w), so a
+      // record's stable slot = start(d) + records of d in earlier warps
+      // (from the final word) + its own warp's earlier records of d (the
+      // atomic's return; the lane/instruction order of one warp's atomics is
+      // verified on the output).  Slot words hold (bin << 16 | position):
+      // the key is rebuilt from the bin, only the value is gathered.
+      const uint32_t nbin = 1u << bits, mask = nbin - 1u, nq = (nbin + 3) >> 2;
+      uint16_t* st16 = reinterpret_cast<uint16_t*>(smem_raw + (cur ? SL::k1 : SL::k0));  // bin starts
+      const uint32_t nib = 4u * (uint32_t)warp;
+      uint32_t rkp[(IPT + 7) / 8];  // own-warp ranks, 4 bits each
+#pragma unroll
+      for (int j = 0; j < (IPT + 7) / 8; ++j) rkp[j] = 0u;
+      bool ovf = false;
+      // (the bins are zero here: zeroed at start and after every span)
+      PH(2)
+#pragma unroll
+      for (int i = 0; i < IPT; ++i) {
+        const uint32_t e = warp * WS + i * 32 + lane;
+        if (e < n) {
+          const uint32_t d = (uint32_t)sk[e] & mask;  // key read right before its atomic
+          const uint32_t r = (atomicAdd(&cnt[d], 1u << nib) >> nib) & 15u;
+          ovf |= r == 15u;
+          rkp[i >> 3] |= r << ((i & 7) * 4);
+        }
+        __syncwarp();
+      }
+      if (ovf) s_big = 1u;  // a warp field would carry: LSD path
+      __syncthreads();
+      PH(3)
+      lsd = s_big != 0u;
+      if (!lsd) {
+        // exclusive scan of the bin totals (sum of the 8 fields) -> st16
+        {
+          const uint32_t qpt = (nq + NT - 1) / NT;
+          const uint32_t q0 = min(nq, tid * qpt), q1 = min(nq, q0 + qpt);
+          const uint4* cq = reinterpret_cast<const uint4*>(cnt);
+          auto tot = [](uint32_t x) {
+            x = (x & 0x0F0F0F0Fu) + ((x >> 4) & 0x0F0F0F0Fu);
+            return (x * 0x01010101u) >> 24;
+          };
+          uint32_t sum = 0;
+          for (uint32_t q = q0; q < q1; ++q) {
+            const uint4 x = cq[q];
+            sum += tot(x.x) + tot(x.y) + tot(x.z) + tot(x.w);
+          }
+          uint32_t incl = sum;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+          }
+          if (lane == 31) s_wt[warp] = incl;
+          __syncthreads();
+          PH(4)
+          uint32_t wp = lane < NW ? s_wt[lane] : 0u;
+#pragma unroll
+          for (int o = 1; o < NW; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, wp, o);
+            if (lane >= o) wp += y;
+          }
+          const uint32_t wex = __shfl_sync(FULL, wp, (warp + 31) & 31);
+          uint32_t base = (warp ? wex : 0u) + incl - sum;
+          for (uint32_t q = q0; q < q1; ++q) {
+            const uint4 x = cq[q];
+            const uint32_t a0 = base, a1 = a0 + tot(x.x), a2 = a1 + tot(x.y), a3 = a2 + tot(x.z);
+            base = a3 + tot(x.w);
+            reinterpret_cast<uint2*>(st16)[q] = make_uint2(a0 | (a1 << 16), a2 | (a3 << 16));
+          }
+        }
+        __syncthreads();
+        PH(5)
+        // slots
+        const uint32_t lowm = (1u << nib) - 1u;  // fields of earlier warps
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          const uint32_t e = warp * WS + i * 32 + lane;
+          if (e < n) {
+            const uint32_t d = (uint32_t)key[i] & mask;
+            uint32_t x = cnt[d] & lowm;
+            x = (x & 0x0F0F0F0Fu) + ((x >> 4) & 0x0F0F0F0Fu);
+            const uint32_t pre = (x * 0x01010101u) >> 24;
+            const uint32_t p = (uint32_t)st16[d] + pre + ((rkp[i >> 3] >> ((i & 7) * 4)) & 15u);
+            si[p] = (d << 16) | e;
+          }
+        }
+        __syncthreads();
+        PH(6)
+        // write-out in slot order (coalesced), checking that positions ascend
+        // inside every bin; a violation re-sorts the bin runs and rewrites
+        const K hi = k0 & ~(K)mask;
+        bool bad = false;
+        for (uint32_t p = tid; p < n; p += NT) {
+          const uint32_t w = si[p];
+          if (p + 1 < n) {
+            const uint32_t nx = si[p + 1];
+            bad |= ((w ^ nx) < 65536u) & (nx < w);
+          }
+          ok[p] = hi | (K)(w >> 16);
+          if (VB) ov[p] = sv[w & 0xffffu];
+        }
+        if (__syncthreads_or(bad) || DTS_FORCE_FIXUP) {
+#if DTS_PHASE_PROF == 2
+          if (tid == 0) atomicAdd(&g_phase[12], 1ull);
+#endif
+          for (uint32_t p = tid; p + 1 < n; p += NT) {
+            const uint32_t x = si[p], y = si[p + 1];
+            const bool lead = (p == 0 || (si[p - 1] >> 16) != (x >> 16)) && (y >> 16) == (x >> 16);
+            if (lead) {
+              const uint32_t b = x >> 16;
+              uint32_t c = 2;
+              while (p + c < n && (si[p + c] >> 16) == b) ++c;
+              for (uint32_t a = 1; a < c; ++a) {
+                const uint32_t w = si[p + a];
+                uint32_t j = a;
+                while (j > 0 && si[p + j - 1] > w) {
+                  si[p + j] = si[p + j - 1];
+                  --j;
+                }
+                si[p + j] = w;
+              }
+            }
+          }
+          __syncthreads();
+          for (uint32_t p = tid; p < n; p += NT) {
+            const uint32_t w = si[p];
+            ok[p] = hi | (K)(w >> 16);
+            if (VB) ov[p] = sv[w & 0xffffu];
+          }
+        }
+        PH(7)
+        // ready for the next span (ordered before its atomics by its first barrier)
+        for (uint32_t q = tid; q < nq; q += NT) reinterpret_cast<uint4*>(cnt)[q] = make_uint4(0u, 0u, 0u, 0u);
+        PH(8)
+        continue;
+      }
+    } else {
+      // ================= counting path on the top CB of more differing bits;
+      // records sharing those bits are ranked by (key, position) ======
+      constexpr int dbits = TL::CB;
+      const int dsh = bits - dbits;
+      const uint32_t nbin = 1u << dbits, mask = nbin - 1u, nwd = (nbin + 1) >> 1;
+      PH(2)
+#pragma unroll
+      for (int i = 0; i < IPT; ++i) {
+        const uint32_t e = warp * WS + i * 32 + lane;
+        if (e < n) {
+          const uint32_t d = (uint32_t)(key[i] >> dsh) & mask;
+          atomicAdd(&cnt[d >> 1], 1u << ((d & 1u) << 4));
+        }
+      }
+      __syncthreads();
+      PH(3)
+      scan_bins(nwd);
       PH(5)
       lsd = s_big != 0u;
       if (!lsd) {
-        // atomic slots (arbitrary order inside a group of equal keys)
+        // atomic slots (arbitrary order inside a group)
         uint16_t* fidx = si16 + TL::CAP;  // final order (second half of si)
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
@@ -250,7 +407,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
         __syncthreads();
         PH(6)
         // stable position = group start + number of group members that
-        // precede the record in the input (groups hold <= FIXMAX records)
+        // precede the record by (key, position) (groups hold <= FIXMAX records)
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
           const uint32_t e = warp * WS + i * 32 + lane;
@@ -259,36 +416,16 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
             const uint32_t end = (cnt[d >> 1] >> ((d & 1u) << 4)) & 0xffffu;
             const uint32_t dp = d - 1u;
             const uint32_t start = d ? (cnt[dp >> 1] >> ((dp & 1u) << 4)) & 0xffffu : 0u;
-            // rank inside the group by (key, position); with dsh == 0 all
-            // keys of a group are equal and only positions count.  The first
-            // four members branch-free (groups hold ~1-2 records), the rest in
-            // a loop.
             uint32_t r = 0;
-            if (dsh == 0) {
-#pragma unroll
-              for (uint32_t q = 0; q < 4; ++q) {
-                const uint32_t x = start + q < end ? (uint32_t)si16[start + q] : 0xFFFFu;
-                r += x < e;
-              }
-              for (uint32_t q = start + 4; q < end; ++q) r += (uint32_t)si16[q] < e;
-            } else {
-              const K me = key[i];
-              for (uint32_t q = start; q < end; ++q) {
-                const uint32_t x = si16[q];
-                const K kx = sk[x];
-                r += (kx < me) || (kx == me && x < e);
-              }
+            const K me = key[i];
+            for (uint32_t q = start; q < end; ++q) {
+              const uint32_t x = si16[q];
+              const K kx = sk[x];
+              r += (kx < me) || (kx == me && x < e);
             }
             fidx[start + r] = (uint16_t)e;
           }
         }
-#if DTS_PHASE_PROF == 2
-        if (tid == 0) {
-          atomicAdd(&g_phase[11], (unsigned long long)bits);
-          atomicAdd(&g_phase[12], 1ull);
-          atomicAdd(&g_phase[13], (unsigned long long)n);
-        }
-#endif
         __syncthreads();
         PH(7)
         for (uint32_t p = tid; p < n; p += NT) {
@@ -296,7 +433,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
           ok[p] = sk[e];
           if (VB) ov[p] = sv[e];
         }
-        for (uint32_t i = tid; i < nwd; i += NT) cnt[i] = 0u;  // ready for the next span
+        zero_bins(nwd);
         __syncthreads();
         PH(8)
         continue;
