@@ -491,7 +491,8 @@ struct Sorter {
     }
     nbc = (nbc + 1) & ~1u;
     const bool wc = wc_env != 0 && nbc <= (uint32_t)WcTile<K, VB>::NBW;
-    const uint64_t BR = wc ? (uint64_t)WcTile<K, VB>::T * WC_LBS : block_records(sizeof(K), VB);
+    static const uint64_t wc_lbs = (uint64_t)std::max(1, env_int("DTS_WC_LBS", (int)WC_LBS));
+    const uint64_t BR = wc ? (uint64_t)WcTile<K, VB>::T * wc_lbs : block_records(sizeof(K), VB);
     const uint64_t TT = wc ? (uint64_t)WcTile<K, VB>::T : (uint64_t)ScatterTile<K, VB>::T;
     // ---- count-matrix shape and hist blocks ----
     std::vector<Blk> blks;

@@ -5,6 +5,10 @@
 
 namespace dts {
 
+#ifndef DTS_LOCAL_REGATOM
+#define DTS_LOCAL_REGATOM 1  // register-sourced rank atomics (order verified on the output)
+#endif
+
 template <typename K, int VB> struct LocalTile {
   // 8 warps: one 4-bit per-warp field per bin in a 32-bit bin word (the
   // stable counting path below); 2 CTAs per SM
@@ -255,12 +259,18 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
       for (int i = 0; i < IPT; ++i) {
         const uint32_t e = warp * WS + i * 32 + lane;
         if (e < n) {
+#if DTS_LOCAL_REGATOM
+          const uint32_t d = (uint32_t)key[i] & mask;
+#else
           const uint32_t d = (uint32_t)sk[e] & mask;  // key read right before its atomic
+#endif
           const uint32_t r = (atomicAdd(&cnt[d], 1u << nib) >> nib) & 15u;
           ovf |= r == 15u;
           rkp[i >> 3] |= r << ((i & 7) * 4);
         }
+#if !DTS_LOCAL_REGATOM
         __syncwarp();
+#endif
       }
       if (ovf) s_big = 1u;  // a warp field would carry: LSD path
       __syncthreads();

@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
 
   for (;;) {
     __syncthreads();
+    PH(7)
     if (tid == 0) s_blk = atomicAdd(ctr, 1u);
     __syncthreads();
     const uint32_t bi = s_blk;
@@ -200,6 +201,7 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       const uint64_t r = len - (uint64_t)kt * T;
       return (uint32_t)(r < (uint64_t)T ? r : (uint64_t)T);
     };
+    PH(9)
     if (tid == 0 && ntl) issue_tile(B.begin, tile_n(0), cur);
     __syncthreads();
     if (tid == 0) s_seg = B.seg;
@@ -506,12 +508,21 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       PH(8)
     }
     // ---- stripe end: flush the unfinished chunks (partial sectors) ----
+    // (C lanes per bucket, one slot each: a warp store covers 32 / C
+    // buckets' runs instead of 32 scattered records)
     __syncthreads();
-    for (uint32_t b = tid; b < nb; b += NT) {
-      const uint2 I = cst[cs * (TL::NBW + 1) + b];
-      for (uint32_t r = I.x >> 16; r < (I.x & 0xffffu); ++r) {
-        st_global(ko_seg + I.y + r, ck[b * CP + r]);
-        if (VB) st_global(vo_seg + I.y + r, cv[b * CP + r]);
+    {
+      constexpr uint32_t BPW = 32 / C;
+      const uint32_t sub = lane / C, r = lane % C;
+      for (uint32_t b0 = warp * BPW; b0 < nb; b0 += NW * BPW) {
+        const uint32_t b = b0 + sub;
+        if (b < nb) {
+          const uint2 I = cst[cs * (TL::NBW + 1) + b];
+          if (r >= (I.x >> 16) && r < (I.x & 0xffffu)) {
+            st_global(ko_seg + I.y + r, ck[b * CP + r]);
+            if (VB) st_global(vo_seg + I.y + r, cv[b * CP + r]);
+          }
+        }
       }
     }
   }

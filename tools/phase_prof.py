@@ -19,7 +19,7 @@ if LOCAL:
     names = ["tma wait", "keys+diff", "zero(-)", "hist", "scan1", "scan2", "slots", "rank barrier", "write-out", "top", "rank (thread 0)"]
 elif os.environ.get("DTS_WC", "1") != "0":
     names = ["stripe/top", "tma wait", "rank", "pair scan", "binfo+map", "placement",
-             "check+write-out", "-", "carry", "-"]
+             "check+write-out", "flush+claim", "carry", "plan+cst"]
 else:
     names = ["top->issue", "issue->bar1", "tma wait", "rank", "prefix+scan", "tst", "placement",
              "lookback", "bar(lookback)", "write-out"]
@@ -36,6 +36,5 @@ print(f"tiles ~{tiles:.0f}  CTA-runs {ctas}  spins {buf[15]}  order-fixes wc {bu
 for i, nm in enumerate(names[:11]):
     print(f"{nm:16s} {buf[i]/tiles:9.0f} cycles/tile  {100*buf[i]/tot:5.1f}%")
 print(f"{'total':16s} {tot/tiles:9.0f} cycles/tile")
-if LOCAL and buf[12]:
-    print(f"counting-path spans {buf[12]}, mean bits {buf[11]/buf[12]:.2f}, mean records {buf[13]/buf[12]:.0f}, "
-          f"rank-loop iterations per record {buf[10]/max(buf[13],1):.2f}")
+if LOCAL:
+    print(f"local-sort spans re-sorted after an order check failure: {buf[12]}")
