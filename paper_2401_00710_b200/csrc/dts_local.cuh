@@ -279,6 +279,9 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
       if (!lsd) {
         // exclusive scan of the bin totals (sum of the 8 fields) -> st16
         {
+          // (<= 2^NB bins: at most QPT quads of 4 bin words per thread, kept
+          // in registers across the barrier)
+          constexpr uint32_t QPT = ((1u << TL::NB) / 4 + NT - 1) / NT;
           const uint32_t qpt = (nq + NT - 1) / NT;
           const uint32_t q0 = min(nq, tid * qpt), q1 = min(nq, q0 + qpt);
           const uint4* cq = reinterpret_cast<const uint4*>(cnt);
@@ -286,10 +289,14 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
             x = (x & 0x0F0F0F0Fu) + ((x >> 4) & 0x0F0F0F0Fu);
             return (x * 0x01010101u) >> 24;
           };
+          uint4 xq[QPT];
+#pragma unroll
+          for (uint32_t j = 0; j < QPT; ++j) xq[j] = q0 + j < q1 ? cq[q0 + j] : make_uint4(0u, 0u, 0u, 0u);
           uint32_t sum = 0;
-          for (uint32_t q = q0; q < q1; ++q) {
-            const uint4 x = cq[q];
-            sum += tot(x.x) + tot(x.y) + tot(x.z) + tot(x.w);
+#pragma unroll
+          for (uint32_t j = 0; j < QPT; ++j) {
+            xq[j] = make_uint4(tot(xq[j].x), tot(xq[j].y), tot(xq[j].z), tot(xq[j].w));
+            sum += xq[j].x + xq[j].y + xq[j].z + xq[j].w;
           }
           uint32_t incl = sum;
 #pragma unroll
@@ -308,11 +315,11 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
           }
           const uint32_t wex = __shfl_sync(FULL, wp, (warp + 31) & 31);
           uint32_t base = (warp ? wex : 0u) + incl - sum;
-          for (uint32_t q = q0; q < q1; ++q) {
-            const uint4 x = cq[q];
-            const uint32_t a0 = base, a1 = a0 + tot(x.x), a2 = a1 + tot(x.y), a3 = a2 + tot(x.z);
-            base = a3 + tot(x.w);
-            reinterpret_cast<uint2*>(st16)[q] = make_uint2(a0 | (a1 << 16), a2 | (a3 << 16));
+#pragma unroll
+          for (uint32_t j = 0; j < QPT; ++j) {
+            const uint32_t a0 = base, a1 = a0 + xq[j].x, a2 = a1 + xq[j].y, a3 = a2 + xq[j].z;
+            base = a3 + xq[j].w;
+            if (q0 + j < q1) reinterpret_cast<uint2*>(st16)[q0 + j] = make_uint2(a0 | (a1 << 16), a2 | (a3 << 16));
           }
         }
         __syncthreads();
