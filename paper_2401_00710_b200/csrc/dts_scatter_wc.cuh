@@ -187,14 +187,18 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
     }
     // per bucket: block offset -> chunk base, hole = fill (carry state kept
     // in cst = {fill | hole << 16, chunk base}, double-buffered across tiles)
+    // chunks are aligned to the key array's absolute 64-byte boundaries (a
+    // segment may start anywhere): offsets count from the aligned base
+    // kout + offset - al, whose first `al` slots the hole logic never writes
     int cs = 0;  // carry-state buffer of the next tile
+    const uint32_t al = (uint32_t)((reinterpret_cast<uintptr_t>(kout + P.offset) / sizeof(K)) & (C - 1));
     for (uint32_t b = tid; b < nb; b += NT) {
-      const uint32_t o = (uint32_t)(scan[P.cnt_base + (uint64_t)b * P.nrows + B.row] - P.scanbase);
+      const uint32_t o = (uint32_t)(scan[P.cnt_base + (uint64_t)b * P.nrows + B.row] - P.scanbase) + al;
       const uint32_t h = o & (uint32_t)(C - 1);
       cst[b] = make_uint2(h | (h << 16), o & ~(uint32_t)(C - 1));
     }
-    K* ko_seg = opaque_ptr(kout + P.offset);
-    V* vo_seg = VB ? opaque_ptr(vout + P.offset) : nullptr;
+    K* ko_seg = opaque_ptr(kout + P.offset - al);
+    V* vo_seg = VB ? opaque_ptr(vout + P.offset - al) : nullptr;
     const uint64_t len = B.end - B.begin;
     const uint32_t ntl = (uint32_t)((len + T - 1) / T);
     auto tile_n = [&](uint32_t kt) {
