@@ -723,8 +723,11 @@ struct Sorter {
   size_t wave_meta_bytes(const HostSeg& s) const {
     const uint64_t BR = block_records(sizeof(K), VB);
     const uint64_t rows = std::max<uint64_t>(1, (s.len + BR - 1) / BR);
-    const uint32_t g = choose_gamma(s.len, W - s.consumed);
-    const uint64_t nbmax = (1u << g) + (1u << std::min(g, gs_max)) + 1u;
+    // (the digit and bucket capacity run_wave will choose)
+    uint32_t g = choose_gamma(s.len, W - s.consumed), gs = 0;
+    uint64_t nbmax = 1u << g;
+    if (cfg.mode == DTS_MODE_DT && sampled_plan(s.len, W - s.consumed, g, gs, s.root && s.consumed == 0))
+      nbmax = (1u << g) + (1u << gs) + 1u;
     const uint64_t tiles = s.len / 2560 + rows + 1;
     return 88 + rows * 28 + nbmax * rows * 12 + (nbmax + 1) * 9 + (1u << g) * 12 + 4096 +
            tiles * (4 + ((nbmax + 1) & ~1ull) * 4);
