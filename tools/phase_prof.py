@@ -10,10 +10,12 @@ n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 10**9
 L = _lib.lib()
 L.dts_debug_phases.restype = ctypes.c_int
 buf = (ctypes.c_ulonglong * 16)()
-g = torch.Generator(device="cuda"); g.manual_seed(0)
-src = torch.randint(0, 10**9, (n,), generator=g, device="cuda", dtype=torch.int64).to(torch.int32)
-k = torch.empty_like(src); v = torch.empty_like(src)
 import os
+CFG = os.environ.get("DTS_CFG", "c2")  # bench.py workload name
+import bench
+from paper_2401_00710_b200 import gen
+src, v0 = gen.generate_device(bench.CONFIGS[CFG], n, 0, "cuda")
+k = torch.empty_like(src); v = torch.empty_like(v0)
 LOCAL = os.environ.get("DTS_PHASE", "1") == "2"
 if LOCAL:
     names = ["tma wait", "keys+diff", "zero(-)", "hist", "scan1", "scan2", "slots", "rank barrier", "write-out", "top", "rank (thread 0)"]
@@ -24,7 +26,7 @@ else:
     names = ["top->issue", "issue->bar1", "tma wait", "rank", "prefix+scan", "tst", "placement",
              "lookback", "bar(lookback)", "write-out"]
 for rep in range(2):
-    k.copy_(src); torch.arange(n, out=v); torch.cuda.synchronize()
+    k.copy_(src); v.copy_(v0); torch.cuda.synchronize()
     L.dts_debug_phases(buf, 16, 1)
     r = sort_device(k, v, SortConfig(), 0, report=True)
     torch.cuda.synchronize()
@@ -37,4 +39,5 @@ for i, nm in enumerate(names[:11]):
     print(f"{nm:16s} {buf[i]/tiles:9.0f} cycles/tile  {100*buf[i]/tot:5.1f}%")
 print(f"{'total':16s} {tot/tiles:9.0f} cycles/tile")
 if LOCAL:
-    print(f"local-sort spans re-sorted after an order check failure: {buf[12]}")
+    print(f"local-sort spans: nibble path {buf[11]}, packed path {buf[10]}, LSD {buf[13]}, "
+          f"all-equal {buf[15]}, re-sorted after an order check failure {buf[12]}")
