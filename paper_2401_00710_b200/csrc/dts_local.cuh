@@ -173,6 +173,9 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
     if (diff) bits = (sizeof(K) == 8) ? 64 - __clzll((long long)diff) : 32 - __clz((int)(uint32_t)diff);
 
     if (bits == 0) {
+#if DTS_PHASE_PROF == 2
+      if (tid == 0) atomicAdd(&g_phase[15], 1ull);
+#endif
       if (S.src) {
         for (uint32_t i = tid; i < n; i += NT) {
           ok[i] = sk[i];
@@ -255,6 +258,9 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
       bool ovf = false;
       // (the bins are zero here: zeroed at start and after every span)
       PH(2)
+#if DTS_PHASE_PROF == 2
+      if (tid == 0) atomicAdd(&g_phase[11], 1ull);
+#endif
 #pragma unroll
       for (int i = 0; i < IPT; ++i) {
         const uint32_t e = warp * WS + i * 32 + lane;
@@ -395,6 +401,9 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
       const int dsh = bits - dbits;
       const uint32_t nbin = 1u << dbits, mask = nbin - 1u, nwd = (nbin + 1) >> 1;
       PH(2)
+#if DTS_PHASE_PROF == 2
+      if (tid == 0) atomicAdd(&g_phase[10], 1ull);
+#endif
 #pragma unroll
       for (int i = 0; i < IPT; ++i) {
         const uint32_t e = warp * WS + i * 32 + lane;
@@ -458,6 +467,9 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
     }
 
     // ================= LSD path: stable passes of <= RB bits ==================
+#if DTS_PHASE_PROF == 2
+      if (tid == 0) atomicAdd(&g_phase[13], 1ull);
+#endif
     uint32_t idx[IPT];
 #pragma unroll
     for (int i = 0; i < IPT; ++i) idx[i] = warp * WS + i * 32 + lane;
