@@ -118,6 +118,25 @@ int dts_partition(const void* keys, const void* vals, uint64_t n,
                   int val_bytes, void* workspace, size_t workspace_bytes,
                   void* stream);
 
+/* Seeded R-MAT edge generator (C5 workload; the reference's edge generator is
+ * generate_edges, gen.py:194-214, Zipf-skewed instead).  Edge i (global index
+ * edge_base + i) descends `scale` levels; at level l a 32-bit draw
+ * u = hi32(splitmix64 mix of (seed, edge, l)) picks quadrant a (u < t0),
+ * b (< t1), c (< t2) or d; src bit = {c,d}, dst bit = {b,d}, MSB first.
+ * dst/src: device arrays of n uint32. */
+int dts_gen_rmat(uint32_t* dst, uint32_t* src, uint64_t n, uint64_t edge_base,
+                 uint64_t seed, int scale, uint32_t t0, uint32_t t1, uint32_t t2,
+                 void* stream);
+
+/* CSR row offsets of ascending keys below nverts (graph transpose after the
+ * sort; reference bench.py:348-349: bincount + cumsum): row_ptr[v] = number
+ * of keys < v for v in [0, nverts] (nverts + 1 device uint64).  EINVAL if the
+ * keys descend or reach nverts.  Blocks on the stream (one flag read). */
+size_t dts_csr_workspace_bytes(uint64_t nverts);
+int dts_csr_offsets(const void* keys, uint64_t n, int key_bytes, uint64_t nverts,
+                    uint64_t* row_ptr, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
 /* Message for the last nonzero status on this thread. */
 const char* dts_last_error(void);
 

@@ -102,6 +102,23 @@ SIGNATURES = (
             ctypes.c_size_t, ctypes.c_void_p,
         ],
     ),
+    (
+        "dts_gen_rmat",
+        ctypes.c_int,
+        [
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+            ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
+        ],
+    ),
+    ("dts_csr_workspace_bytes", ctypes.c_size_t, [ctypes.c_uint64]),
+    (
+        "dts_csr_offsets",
+        ctypes.c_int,
+        [
+            ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64, ctypes.c_void_p,
+            ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+        ],
+    ),
     ("dts_last_error", ctypes.c_char_p, []),
     ("dts_abi_version", ctypes.c_int, []),
     ("dts_build_arch", ctypes.c_int, []),

@@ -20,6 +20,7 @@
 #include "dts_local.cuh"
 #include "dts_scatter.cuh"
 #include "dts_scatter_wc.cuh"
+#include "dts_graph.cuh"
 
 using namespace dts;
 
@@ -1221,6 +1222,49 @@ int dts_partition(const void* keys, const void* vals, uint64_t n, uint64_t gbase
   if (vb == 0) return partition_impl<uint64_t, 0>(keys, vals, n, gbase, split_keys, split_idx, nsplit, okeys, ovals, counts, ws, wsb, st);
   if (vb == 4) return partition_impl<uint64_t, 4>(keys, vals, n, gbase, split_keys, split_idx, nsplit, okeys, ovals, counts, ws, wsb, st);
   return partition_impl<uint64_t, 8>(keys, vals, n, gbase, split_keys, split_idx, nsplit, okeys, ovals, counts, ws, wsb, st);
+}
+
+int dts_gen_rmat(uint32_t* dst, uint32_t* src, uint64_t n, uint64_t edge_base, uint64_t seed, int scale,
+                 uint32_t t0, uint32_t t1, uint32_t t2, void* stream) {
+  if (scale < 1 || scale > 32) return fail(DTS_EINVAL, "scale must be in [1, 32]");
+  if (!(t0 <= t1 && t1 <= t2)) return fail(DTS_EINVAL, "quadrant thresholds must be non-decreasing");
+  if (n == 0) return 0;
+  if (!dst || !src) return fail(DTS_EINVAL, "dst and src must not be NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 64);
+  k_gen_rmat<<<(unsigned)blocks, 256, 0, st>>>(dst, src, n, edge_base, seed, (uint32_t)scale, t0, t1, t2);
+  return check_launch("k_gen_rmat");
+}
+
+size_t dts_csr_workspace_bytes(uint64_t nverts) { return 256 + 24 * (size_t)(nverts / CSR_LONG + 2); }
+
+int dts_csr_offsets(const void* keys, uint64_t n, int kb, uint64_t nverts, uint64_t* row_ptr, void* ws, size_t wsb,
+                    void* stream) {
+  if (kb != 4 && kb != 8) return fail(DTS_EINVAL, "key_bytes must be 4|8");
+  if (!row_ptr) return fail(DTS_EINVAL, "row_ptr must not be NULL");
+  if (n && !keys) return fail(DTS_EINVAL, "keys must not be NULL");
+  if (wsb < dts_csr_workspace_bytes(nverts) || !ws) return fail(DTS_ENOMEM, "workspace too small for dts_csr_offsets");
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* flags = (uint32_t*)ws;  // [0] gap count, [1] bad
+  uint64_t* gaps = (uint64_t*)((char*)ws + 256);
+  const uint32_t cap = (uint32_t)std::min<uint64_t>((wsb - 256) / 24, 0xFFFFFFFFull);
+  CUDA_TRY(cudaMemsetAsync(flags, 0, 8, st));
+  const uint64_t blocks = std::min<uint64_t>((n + 1 + 255) / 256, 148ull * 64);
+  if (kb == 4)
+    k_csr_offsets<uint32_t><<<(unsigned)blocks, 256, 0, st>>>((const uint32_t*)keys, n, nverts, row_ptr, gaps, flags, cap, flags + 1);
+  else
+    k_csr_offsets<uint64_t><<<(unsigned)blocks, 256, 0, st>>>((const uint64_t*)keys, n, nverts, row_ptr, gaps, flags, cap, flags + 1);
+  DTS_TRY(check_launch("k_csr_offsets"));
+  uint32_t h[2];
+  CUDA_TRY(cudaMemcpyAsync(h, flags, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (h[1] == 1u) return fail(DTS_EINVAL, "keys must be ascending and below nverts");
+  if (h[1] == 2u) return fail(DTS_ENOMEM, "workspace too small for the CSR gap list");
+  if (h[0]) {
+    k_csr_fill_gaps<<<h[0], 256, 0, st>>>(gaps, flags, row_ptr);
+    DTS_TRY(check_launch("k_csr_fill_gaps"));
+  }
+  return 0;
 }
 
 const char* dts_last_error(void) { return g_err.c_str(); }

@@ -390,7 +390,12 @@ __global__ void __launch_bounds__(256) k_copy_ranges(const CopyR* __restrict__ r
   auto col = [&](auto* dst, const auto* src, uint64_t off, uint32_t len) {
     using E = typename std::remove_const<typename std::remove_pointer<decltype(src)>::type>::type;
     constexpr uint32_t VEC = 16 / sizeof(E);
-    const uint32_t head = (uint32_t)((VEC - (off % VEC)) % VEC) < len ? (uint32_t)((VEC - (off % VEC)) % VEC) : len;
+    // (the caller's column may start anywhere: vectors only when both ends
+    // share their 16-byte phase, head taken from the destination address)
+    const uintptr_t da = reinterpret_cast<uintptr_t>(dst + off), sa = reinterpret_cast<uintptr_t>(src + off);
+    const bool vec_ok = ((da ^ sa) & 15u) == 0;
+    const uint32_t h0 = (uint32_t)(((16u - (da & 15u)) & 15u) / sizeof(E));
+    const uint32_t head = !vec_ok ? len : (h0 < len ? h0 : len);
     const uint32_t nv = (len - head) / VEC;
     for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) dst[off + i] = src[off + i];
     const uint4* s4 = reinterpret_cast<const uint4*>(src + off + head);

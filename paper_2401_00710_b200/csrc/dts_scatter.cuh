@@ -47,12 +47,13 @@ template <typename K, int VB, bool SPLIT> struct ScatterSmem {
 };
 
 // Split [g0, g0+tn) of a T-typed column into head / 16-byte aligned body /
-// tail; returns the body bytes (moved by cp.async.bulk).
+// tail by absolute address (the caller's column may start anywhere); returns
+// the body bytes (moved by cp.async.bulk).
 template <typename T>
-__device__ __forceinline__ uint32_t tile_body(uint64_t g0, uint32_t tn, uint32_t& off,
+__device__ __forceinline__ uint32_t tile_body(const T* col, uint64_t g0, uint32_t tn, uint32_t& off,
                                               uint32_t& head, uint32_t& nbody) {
   constexpr uint32_t VEC = 16 / sizeof(T);
-  off = (uint32_t)(g0 % VEC);
+  off = (uint32_t)((reinterpret_cast<uintptr_t>(col + g0) & 15u) / sizeof(T));
   const uint32_t h0 = (VEC - off) % VEC;
   head = h0 < tn ? h0 : tn;
   nbody = ((tn - head) / VEC) * VEC;
@@ -399,10 +400,10 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
       if (lane == 0) {
         const TileGeo& N = sgeo[cur ^ 1];
         uint32_t o2, h2, b2;
-        const uint32_t kb2 = tile_body<K>(N.g0, N.tn, o2, h2, b2);
+        const uint32_t kb2 = tile_body<K>(kin, N.g0, N.tn, o2, h2, b2);
         if (kb2) prefetch_l2(kin + N.g0 + h2, kb2);
         if (VB) {
-          const uint32_t vb2 = tile_body<V>(N.g0, N.tn, o2, h2, b2);
+          const uint32_t vb2 = tile_body<V>(vin, N.g0, N.tn, o2, h2, b2);
           if (vb2) prefetch_l2(vin + N.g0 + h2, vb2);
         }
       }

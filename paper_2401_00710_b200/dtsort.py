@@ -9,6 +9,7 @@ in libdts.so (include/dts.h `dts_sort`) on the current CUDA stream.
 from __future__ import annotations
 
 import ctypes
+import os
 
 from . import _lib
 from ._device import Column, pick_device, torch_mod
@@ -69,6 +70,63 @@ def report_from(raw: _lib.DtsReport) -> InstrumentReport:
     return rep
 
 
+# One dts_sort call keeps 32-bit positions inside a segment; larger inputs
+# are split first (DTS_SPLIT_N lowers the bound for tests).
+def split_n() -> int:
+    return int(os.environ.get("DTS_SPLIT_N", (1 << 32) - (1 << 16)))
+
+
+def _merge_reports(reps, n: int, extra_launches: int) -> InstrumentReport:
+    out = InstrumentReport()
+    out.levels = max(r.levels for r in reps)
+    out.skipped_bits = max(r.skipped_bits for r in reps)
+    for f in ("moves", "merge_out_copies", "merge_in_array_moves", "base_case_records", "records_distributed",
+              "gpu_launches"):
+        setattr(out, f, sum(getattr(r, f) for r in reps))
+    out.gpu_launches += extra_launches
+    depth = max(len(r.level_mass) for r in reps)
+    out.level_mass = [sum(r.level_mass[d] for r in reps if d < len(r.level_mass)) for d in range(depth)]
+    out.level_mass[0] = n
+    hd = max(len(r.heavy_records_removed) for r in reps)
+    out.heavy_records_removed = [sum(r.heavy_records_removed[d] for r in reps if d < len(r.heavy_records_removed))
+                                 for d in range(hd)]
+    out.kernel_ms = {k: sum(r.kernel_ms[k] for r in reps) for k in reps[0].kernel_ms}
+    out.kernel_launches = {k: sum(r.kernel_launches[k] for r in reps) for k in reps[0].kernel_launches}
+    out.kernel_records = {k: sum(r.kernel_records[k] for r in reps) for k in reps[0].kernel_records}
+    return out
+
+
+def _sort_split(keys, vals, cfg: SortConfig, mode: int, profile: bool, report: bool):
+    """n >= SPLIT_N on one GPU: the multi-GPU algorithm without the exchange
+    (distributed.py): G-1 composite (key, index) splitters from a sample, one
+    stable G-way dts_partition, then dts_sort of every part in place; parts
+    are key ranges in order and keep input order, so the result is the
+    stable sort."""
+    from .distributed import CudaOps, choose_splitters
+
+    n = int(keys.numel())
+    SPLIT_N = split_n()
+    G = max(2, -(-n // (SPLIT_N // 2)))
+    ops = CudaOps(cfg, mode)
+    sk, si = ops.sample(keys, 0, min(n, 4096 * G), cfg.seed)
+    spk, spi = choose_splitters(sk, si, G)
+    pk, pv, counts = ops.partition(keys, vals, 0, spk, spi)
+    if max(counts) >= SPLIT_N:
+        raise RuntimeError(f"split sort: a part of {max(counts)} records exceeds {SPLIT_N}")
+    reps, off = [], 0
+    for c in counts:
+        if c:
+            r = sort_device(pk[off:off + c], None if pv is None else pv[off:off + c], cfg, mode, profile,
+                            report=report or cfg.instrument or profile)
+            if r is not None:
+                reps.append(r)
+        off += c
+    keys.copy_(pk)
+    if vals is not None:
+        vals.copy_(pv)
+    return _merge_reports(reps, n, 6) if reps else None
+
+
 def sort_device(keys, vals, cfg: SortConfig, mode: int, profile: bool = False,
                 workspace=None, report: bool = False) -> InstrumentReport | None:
     """Sort contiguous CUDA tensors in place (no validation beyond widths).
@@ -79,6 +137,8 @@ def sort_device(keys, vals, cfg: SortConfig, mode: int, profile: bool = False,
     """
     torch = torch_mod()
     n = int(keys.numel())
+    if n >= split_n():
+        return _sort_split(keys, vals, cfg, mode, profile, report)
     kb = keys.element_size()
     vb = 0 if vals is None else vals.element_size()
     c = make_config(cfg, mode, profile)

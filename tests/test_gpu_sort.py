@@ -205,3 +205,27 @@ def test_gpu_large_c2_certificate():
     assert bool((v[1:][eq] > v[:-1][eq]).all())
     assert bool((k0[v.long()] == k).all())
     assert int(torch.bincount(v.long(), minlength=n).max()) == 1
+
+
+@pytest.mark.parametrize("kb,vb", [(4, 4), (8, 8), (4, 8)])
+@pytest.mark.parametrize("shift", [1, 2, 3])
+def test_gpu_unaligned_device_slices(kb, vb, shift):
+    """Caller columns that start off any 16-byte boundary (tensor slices):
+    every kernel must address them by absolute alignment."""
+    import torch
+
+    from paper_2401_00710_b200 import RecordArray, dt_sort
+
+    rng = np.random.default_rng(shift)
+    n = 300_007
+    kd = np.uint32 if kb == 4 else np.uint64
+    vd = np.uint32 if vb == 4 else np.uint64
+    keys = rng.integers(0, 1 << 24, n + shift).astype(kd)
+    keys[rng.random(n + shift) < 0.2] = 5  # heavy key: finished runs are copied T -> A
+    vals = np.arange(n + shift, dtype=vd)
+    tk = torch.from_numpy(keys.copy()).cuda()
+    tv = torch.from_numpy(vals.copy()).cuda()
+    dt_sort(RecordArray(tk[shift:], tv[shift:]))
+    wk, wv = ora.dt_sort(keys[shift:].copy(), vals[shift:].copy())
+    assert np.array_equal(tk[shift:].cpu().numpy(), wk) and np.array_equal(tv[shift:].cpu().numpy(), wv)
+    assert np.array_equal(tk[:shift].cpu().numpy(), keys[:shift])  # untouched prefix
