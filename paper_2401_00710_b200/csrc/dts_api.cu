@@ -62,6 +62,14 @@ constexpr uint32_t COPY_CHUNK = 1u << 16;
 // (dtsort.py:225); here small segments skip it: heavy keys found there save
 // little, and each sampled segment costs a sample sort (output unaffected).
 constexpr uint64_t SAMPLE_FACTOR = 32;
+// ... and, below the root, small segments (< SAMPLE_MIN records) only when
+// their parent had heavy keys or the level has <= SAMPLE_MANY segments: a
+// heavy key of a small segment saves at most one small pass, while every
+// sampled segment costs a sample sort, a plan read-back and host planning
+// (C4 level 2: 0.6-1.3 x 10^5 segments of ~6-16 K records); skewed inputs
+// (Zipf) keep finding heavy keys level after level in fewer segments
+constexpr uint64_t SAMPLE_MIN = 1u << 17;
+constexpr size_t SAMPLE_MANY = 8192;
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -303,12 +311,13 @@ struct Sorter {
   // and returns the subsample exponent gs (|S| = 2^gs * stride).
   // Below the root the strided subsample has <= 2^7 entries (heavy keys of
   // >= 1/128 of a segment): each sampled segment sorts its sample in one CTA.
-  bool sampled_plan(uint64_t len, uint32_t remaining, uint32_t& g, uint32_t& gs, bool root) const {
+  bool sampled_plan(uint64_t len, uint32_t remaining, uint32_t& g, uint32_t& gs, bool root,
+                    bool small_ok) const {
     const uint32_t g9 = std::min<uint32_t>(g, gcap_hw > 1 ? gcap_hw - 1 : 1);
     gs = std::min<uint32_t>(g9 > 1 ? g9 - 1 : 1, root ? gs_max : std::min<uint32_t>(gs_max, 7));
     uint64_t S = std::min<uint64_t>(len, (uint64_t(1) << gs) * stride);
     S = std::min<uint64_t>(S, smax);
-    if (len < SAMPLE_FACTOR * S) return false;
+    if (len < SAMPLE_FACTOR * S || (!root && !small_ok && len < SAMPLE_MIN)) return false;
     g = std::min(g9, remaining);
     gs = std::min<uint32_t>(gs, g > 1 ? g - 1 : 1);
     return true;
@@ -426,14 +435,15 @@ struct Sorter {
       P.nb = 1u << g;
       P.nbmax = P.nb;
       uint32_t gs = 0;
-      if (dt && sampled_plan(hs.len, remaining, g, gs, hs.root && hs.consumed == 0)) {
+      if (dt && sampled_plan(hs.len, remaining, g, gs, (hs.root & 1u) && hs.consumed == 0,
+                             (hs.root & 2u) != 0 || segs.size() <= SAMPLE_MANY)) {
         // sampled segments may gain heavy / overflow buckets; the digit is
         // capped so bucket ids stay below the scatter's 2^10 capacity
         P.gamma = g;
         P.shift = remaining - g;
         P.flags |= PF_SAMPLE;
         P.sample_gs = gs;
-        if (hs.root && hs.consumed == 0) P.flags |= PF_ROOTSKIP;
+        if ((hs.root & 1u) && hs.consumed == 0) P.flags |= PF_ROOTSKIP;
         P.nb = 1u << g;
         P.nbmax = (1u << g) + (1u << gs) + 1u;
         P.heavy_base = (uint32_t)heavy_total;
@@ -721,13 +731,15 @@ struct Sorter {
     return 0;
   }
 
-  size_t wave_meta_bytes(const HostSeg& s) const {
+  size_t wave_meta_bytes(const HostSeg& s, size_t level_segs) const {
     const uint64_t BR = block_records(sizeof(K), VB);
     const uint64_t rows = std::max<uint64_t>(1, (s.len + BR - 1) / BR);
     // (the digit and bucket capacity run_wave will choose)
     uint32_t g = choose_gamma(s.len, W - s.consumed), gs = 0;
     uint64_t nbmax = 1u << g;
-    if (cfg.mode == DTS_MODE_DT && sampled_plan(s.len, W - s.consumed, g, gs, s.root && s.consumed == 0))
+    if (cfg.mode == DTS_MODE_DT &&
+        sampled_plan(s.len, W - s.consumed, g, gs, (s.root & 1u) && s.consumed == 0,
+                     (s.root & 2u) != 0 || level_segs <= SAMPLE_MANY))
       nbmax = (1u << g) + (1u << gs) + 1u;
     const uint64_t tiles = s.len / 2560 + rows + 1;
     return 88 + rows * 28 + nbmax * rows * 12 + (nbmax + 1) * 9 + (1u << g) * 12 + 4096 +
@@ -752,7 +764,7 @@ struct Sorter {
       while (s0 < segs.size()) {
         size_t s1 = s0, need = 1 << 16;
         while (s1 < segs.size()) {
-          const size_t b = wave_meta_bytes(segs[s1]);
+          const size_t b = wave_meta_bytes(segs[s1], segs.size());
           if (s1 > s0 && need + b > budget) break;
           need += b;
           ++s1;

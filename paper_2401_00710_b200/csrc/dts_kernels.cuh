@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(256) k_copy_ranges(const CopyR* __restrict__ r
 // ---------------------------------------------------------------------------
 struct NextSeg {
   uint64_t offset, len;
-  uint32_t consumed, pad;
+  uint32_t consumed, pad;  // pad: bit 0 root (host only), bit 1 parent had heavy keys
 };
 
 constexpr int CLS_NT = 256;
@@ -577,7 +577,9 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(const SegPlan* __restrict__
       const uint64_t lo = P.offset + s_bs[b], sz = s_bs[b + 1] - s_bs[b];
       const uint8_t kind = kinds[P.bs_base + b];
       const uint32_t rem = kind == KIND_OVF ? W : P.shift;
-      next[s_base[2] + atomicAdd(&s_n[2], 1u)] = NextSeg{lo, sz, W - rem, 0u};
+      // pad bit 1: the parent segment had heavy keys (its children are
+      // sampled even when small, dts_api.cu SAMPLE_MIN)
+      next[s_base[2] + atomicAdd(&s_n[2], 1u)] = NextSeg{lo, sz, W - rem, P.nheavy ? 2u : 0u};
     }
   }
 }
