@@ -619,7 +619,33 @@ struct Sorter {
       tm.end(ev, bs_total);
       DTS_TRY(check_launch("k_bucket_bounds"));
     }
-    // ---- scatter ----
+    // ---- classify buckets on the device (dtsort.py:244-318 _children_step)
+    // from the bucket bounds; the scatter, the base case and the copies
+    // follow; only the counters, the (few) next-level segments and the plans
+    // come back ----
+    const uint32_t out_src = in_T ? 0u : 1u;  // where the scatter wrote
+    const uint64_t cap_copy = bs_total + wave_recs / COPY_CHUNK + 1;
+    Span* dspan = (Span*)meta.take(std::max<uint64_t>(1, bs_total) * sizeof(Span));
+    CopyR* dcopy = (CopyR*)meta.take(cap_copy * sizeof(CopyR));
+    NextSeg* dnext = (NextSeg*)meta.take(std::max<uint64_t>(1, bs_total) * sizeof(NextSeg));
+    unsigned long long* dcc = (unsigned long long*)meta.take(8 * sizeof(unsigned long long));
+    if (!dspan || !dcopy || !dnext || !dcc) return fail(DTS_ENOMEM, "workspace too small for level metadata");
+    CUDA_TRY(cudaMemsetAsync(dcc, 0, 8 * sizeof(unsigned long long), st));
+    k_classify<<<(unsigned)ns, CLS_NT, 0, st>>>(dplans, dbs, dkinds, (uint32_t)W, out_src, thr, COPY_CHUNK,
+                                           dspan, dcopy, dnext, dcc);
+    tm.launches += 1;
+    DTS_TRY(check_launch("k_classify"));
+    constexpr uint64_t NEXT_CAP = 4096;  // next segments returned with the counters
+    const uint64_t ncap = std::min<uint64_t>(NEXT_CAP, std::max<uint64_t>(1, bs_total));
+    DTS_TRY(g_pin_back.ensure(256 + align256(pb) + ncap * sizeof(NextSeg) + 256));
+    char* bp = (char*)g_pin_back.p;
+    CUDA_TRY(cudaMemcpyAsync(bp, dcc, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(bp + 256, dplans, pb, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(bp + 256 + align256(pb), dnext, ncap * sizeof(NextSeg),
+                             cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(ev_cls, st));
+    // ---- scatter (after the classifier: it only needs the bucket bounds,
+    // so the host receives the next level while the scatter runs) ----
     if (wc) {
       CUDA_TRY(cudaMemsetAsync(dctr + 1, 0, 4, st));
       Timer::Ev ev;
@@ -647,30 +673,6 @@ struct Sorter {
       tm.end(ev, wave_recs);
       DTS_TRY(check_launch("k_scatter"));
     }
-    // ---- classify buckets on the device (dtsort.py:244-318 _children_step),
-    // then the base case and the copies straight away; only the counters,
-    // the (few) next-level segments and the plans come back ----
-    const uint32_t out_src = in_T ? 0u : 1u;  // where the scatter wrote
-    const uint64_t cap_copy = bs_total + wave_recs / COPY_CHUNK + 1;
-    Span* dspan = (Span*)meta.take(std::max<uint64_t>(1, bs_total) * sizeof(Span));
-    CopyR* dcopy = (CopyR*)meta.take(cap_copy * sizeof(CopyR));
-    NextSeg* dnext = (NextSeg*)meta.take(std::max<uint64_t>(1, bs_total) * sizeof(NextSeg));
-    unsigned long long* dcc = (unsigned long long*)meta.take(8 * sizeof(unsigned long long));
-    if (!dspan || !dcopy || !dnext || !dcc) return fail(DTS_ENOMEM, "workspace too small for level metadata");
-    CUDA_TRY(cudaMemsetAsync(dcc, 0, 8 * sizeof(unsigned long long), st));
-    k_classify<<<(unsigned)ns, CLS_NT, 0, st>>>(dplans, dbs, dkinds, (uint32_t)W, out_src, thr, COPY_CHUNK,
-                                           dspan, dcopy, dnext, dcc);
-    tm.launches += 1;
-    DTS_TRY(check_launch("k_classify"));
-    constexpr uint64_t NEXT_CAP = 4096;  // next segments returned with the counters
-    const uint64_t ncap = std::min<uint64_t>(NEXT_CAP, std::max<uint64_t>(1, bs_total));
-    DTS_TRY(g_pin_back.ensure(256 + align256(pb) + ncap * sizeof(NextSeg) + 256));
-    char* bp = (char*)g_pin_back.p;
-    CUDA_TRY(cudaMemcpyAsync(bp, dcc, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(bp + 256, dplans, pb, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(bp + 256 + align256(pb), dnext, ncap * sizeof(NextSeg),
-                             cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaEventRecord(ev_cls, st));
     {
       Timer::Ev ev;
       tm.begin(DTS_K_LOCAL, ev);
