@@ -42,7 +42,7 @@ template <typename K, int VB> struct WcTile {
   static constexpr int NT = 512;
   static constexpr int NW = NT / 32;
   static constexpr int PT = 1;  // threads per bucket pair in the pair phases
-  static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? 9 : 5;
+  static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? 11 : 6;
   static constexpr int WS = 32 * IPT;
   static constexpr int T = NT * IPT;
   static constexpr int NBW = 520;  // bucket capacity (2^9 light + overflow + slack)
