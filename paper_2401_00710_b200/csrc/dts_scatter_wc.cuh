@@ -42,7 +42,7 @@ template <typename K, int VB> struct WcTile {
   static constexpr int NT = 512;
   static constexpr int NW = NT / 32;
   static constexpr int PT = 1;  // threads per bucket pair in the pair phases
-  static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? 11 : 6;
+  static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? 12 : 6;
   static constexpr int WS = 32 * IPT;
   static constexpr int T = NT * IPT;
   static constexpr int NBW = 520;  // bucket capacity (2^9 light + overflow + slack)
@@ -65,7 +65,7 @@ template <typename K, int VB> struct WcSmem {
   // per chunk of the tile: {dest of slot 0, staging index of slot 0,
   // carry slots | hole << 8, bucket}
   static constexpr size_t cd = a16(wh + (size_t)TL::NW * (TL::NBW / 2) * 4);
-  static constexpr size_t nf = a16(cd + (size_t)TL::MAXCH * 16);       // carry copy descriptors
+  static constexpr size_t nf = a16(cd + (size_t)TL::MAXCH * 8);        // carry copy descriptors
   static constexpr size_t cst = a16(nf + (size_t)TL::NBW * 4);         // 2 x carry state
   static constexpr size_t hk = a16(cst + (size_t)2 * (TL::NBW + 1) * 8);
   static constexpr size_t hz = a16(hk + (size_t)TL::HKC * sizeof(K));
@@ -115,7 +115,10 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
   K* ck = reinterpret_cast<K*>(smem_raw + SL::ck);
   V* cv = reinterpret_cast<V*>(smem_raw + SL::cv);
   uint32_t* wh = reinterpret_cast<uint32_t*>(smem_raw + SL::wh);
-  uint4* cdesc = reinterpret_cast<uint4*>(smem_raw + SL::cd);
+  // chunk descriptor: {dest of slot 0, staging index of slot 0 + 16 (14 bits)
+  // | carry slots << 14 | hole << 18 | bucket << 22}
+  uint2* cdesc = reinterpret_cast<uint2*>(smem_raw + SL::cd);
+  static_assert(TL::T + 2 * C + 16 < (1 << 14) && TL::NBW <= 1024 && C <= 16, "packed chunk descriptors");
   uint32_t* bnf = reinterpret_cast<uint32_t*>(smem_raw + SL::nf);  // copy: src | dst<<16 | cnt<<24
   uint2* cst = reinterpret_cast<uint2*>(smem_raw + SL::cst);      // {fill | hole << 16, chunk base}
   K* hk = reinterpret_cast<K*>(smem_raw + SL::hk);
@@ -368,7 +371,7 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
           auto chunks = [&](uint32_t b, uint2 I, uint32_t f, uint32_t t, uint32_t g0) {
             const uint32_t cc = I.x & 0xffffu, ch = I.x >> 16;
             for (uint32_t k = 0; k < f; ++k)
-              cdesc[g0 + k] = make_uint4(I.y + k * C, t - cc + k * C, k ? 0u : (cc | (ch << 8)), b);
+              cdesc[g0 + k] = make_uint2(I.y + k * C, (t - cc + k * C + 16u) | (k ? 0u : ((cc << 14) | (ch << 18))) | (b << 22));
           };
           if (pq == 0) {
             next(2 * pj, I0, n0, f0, t0);
@@ -412,16 +415,17 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       auto write_chunks = [&]() {
         const uint32_t nslot = nch * C;
         for (uint32_t q = tid; q < nslot; q += NT) {
-          const uint4 D = cdesc[q / C];
+          const uint2 D = cdesc[q / C];
           const uint32_t r = q % C;
-          if (r < ((D.z >> 8) & 0xffu)) continue;  // hole: the previous stripe's records
+          if (r < ((D.y >> 18) & 15u)) continue;  // hole: the previous stripe's records
           K kk;
           V vv = V(0);
-          if (r < (D.z & 0xffu)) {
-            kk = ck[D.w * CP + r];
-            if (VB) vv = cv[D.w * CP + r];
+          if (r < ((D.y >> 14) & 15u)) {
+            const uint32_t b = D.y >> 22;
+            kk = ck[b * CP + r];
+            if (VB) vv = cv[b * CP + r];
           } else {
-            st_get(D.y + r, kk, vv);
+            st_get((D.y & 0x3FFFu) - 16u + r, kk, vv);
           }
           const uint32_t d = D.x + r;
           st_global(ko_seg + d, kk);
