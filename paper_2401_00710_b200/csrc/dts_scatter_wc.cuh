@@ -42,12 +42,12 @@ template <typename K, int VB> struct WcTile {
   static constexpr int NT = 512;
   static constexpr int NW = NT / 32;
   static constexpr int PT = 1;  // threads per bucket pair in the pair phases
-  static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? 12 : 6;
+  static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? 14 : 7;
   static constexpr int WS = 32 * IPT;
   static constexpr int T = NT * IPT;
   static constexpr int NBW = 520;  // bucket capacity (2^9 light + overflow + slack)
   static constexpr int C = (sizeof(K) == 8 || VB == 8) ? 8 : 16;  // chunk records (64 B)
-  static constexpr int CP = C + 1;                                 // carry stride (banks)
+  static constexpr int CP = C;  // carry stride (unpadded: the two half-warp runs of a carry step conflict at most 2-way)
   static constexpr int MAXCH = (T + (C - 1) * NBW) / C + 2;       // chunks per tile bound
   static constexpr int HKC = 256;
   static constexpr int HZC = 520;
@@ -58,16 +58,17 @@ template <typename K, int VB> struct WcSmem {
   static constexpr size_t kb = a16((size_t)(TL::T + 8) * sizeof(K));
   static constexpr size_t vb = a16((size_t)(TL::T + 8) * VB);
   static constexpr size_t buf = 0;                                   // 2 x (keys | vals)
-  static constexpr size_t pk = a16(buf + 2 * (kb + vb));             // staging (b<<16|e)
-  static constexpr size_t ck = a16(pk + (size_t)(TL::T + 1) * 4);    // carry keys
+  static constexpr size_t pk = a16(buf + 2 * (kb + vb));             // staging: tile position (u16)
+  static constexpr size_t be = a16(pk + (size_t)(TL::T + 2) * 2);    // staging: bucket-run end bits
+  static constexpr size_t ck = a16(be + (size_t)(TL::T / 32 + 2) * 4);  // carry keys
   static constexpr size_t cv = a16(ck + (size_t)TL::NBW * TL::CP * sizeof(K));
   static constexpr size_t wh = a16(cv + (size_t)TL::NBW * TL::CP * VB);  // per-warp counters
   // per chunk of the tile: {dest of slot 0, staging index of slot 0,
   // carry slots | hole << 8, bucket}
   static constexpr size_t cd = a16(wh + (size_t)TL::NW * (TL::NBW / 2) * 4);
   static constexpr size_t nf = a16(cd + (size_t)TL::MAXCH * 8);        // carry copy descriptors
-  static constexpr size_t cst = a16(nf + (size_t)TL::NBW * 4);         // 2 x carry state
-  static constexpr size_t hk = a16(cst + (size_t)2 * (TL::NBW + 1) * 8);
+  static constexpr size_t cst = a16(nf + (size_t)TL::NBW * 4);         // carry state
+  static constexpr size_t hk = a16(cst + (size_t)(TL::NBW + 1) * 8);
   static constexpr size_t hz = a16(hk + (size_t)TL::HKC * sizeof(K));
   static constexpr size_t plan = a16(hz + (size_t)TL::HZC * 4);
   static constexpr size_t bar = a16(plan + sizeof(SegPlan));
@@ -111,7 +112,8 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
   static_assert(HW * PT <= (uint32_t)NT, "PT threads per bucket pair");
   static_assert(T < 65536, "packed u16 counts");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* pk = reinterpret_cast<uint32_t*>(smem_raw + SL::pk);
+  uint16_t* pk = reinterpret_cast<uint16_t*>(smem_raw + SL::pk);
+  uint32_t* bend = reinterpret_cast<uint32_t*>(smem_raw + SL::be);  // bit p: slot p ends a bucket run
   K* ck = reinterpret_cast<K*>(smem_raw + SL::ck);
   V* cv = reinterpret_cast<V*>(smem_raw + SL::cv);
   uint32_t* wh = reinterpret_cast<uint32_t*>(smem_raw + SL::wh);
@@ -189,11 +191,11 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       for (uint32_t i = tid; i < P.nheavy && i < (uint32_t)TL::HKC; i += NT) hk[i] = heavy_pool[P.heavy_base + i];
     }
     // per bucket: block offset -> chunk base, hole = fill (carry state kept
-    // in cst = {fill | hole << 16, chunk base}, double-buffered across tiles)
+    // in cst = {fill | hole << 16, chunk base}: read by each bucket pair's
+    // owner in the pair phase, rewritten by it after the next barrier)
     // chunks are aligned to the key array's absolute 64-byte boundaries (a
     // segment may start anywhere): offsets count from the aligned base
     // kout + offset - al, whose first `al` slots the hole logic never writes
-    int cs = 0;  // carry-state buffer of the next tile
     const uint32_t al = (uint32_t)((reinterpret_cast<uintptr_t>(kout + P.offset) / sizeof(K)) & (C - 1));
     for (uint32_t b = tid; b < nb; b += NT) {
       const uint32_t o = (uint32_t)(scan[P.cnt_base + (uint64_t)b * P.nrows + B.row] - P.scanbase) + al;
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
     __syncthreads();
     if (tid == 0) s_seg = B.seg;
 
-    for (uint32_t kt = 0; kt < ntl; ++kt, cur ^= 1, cs ^= 1) {
+    for (uint32_t kt = 0; kt < ntl; ++kt, cur ^= 1) {
       PH(0)
       const uint32_t tn = tile_n(kt);
       const bool full = tn == (uint32_t)T;
@@ -251,6 +253,9 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       const K* ik = xk + s_off[cur][0];
       const V* iv = xv + s_off[cur][1];
 
+      // (run-end bits of this tile: set in the pair phase below; the last
+      // reads of the previous tile's were before its write-out barrier)
+      for (uint32_t i = tid; i < (uint32_t)(T / 32 + 2); i += NT) bend[i] = 0u;
       // ---- route + per-warp rank; records into registers ----
       K key[IPT];
       V val[IPT];
@@ -292,14 +297,13 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       // the other buffer (previous tile's staging) is free: stream the next tile
       if (tid == 0) {
         if (kt + 1 < ntl) issue_tile(B.begin + (uint64_t)(kt + 1) * T, tile_n(kt + 1), cur ^ 1);
-        pk[tn] = 0xFFFFFFFFu;  // order-check sentinel
       }
 
       // ---- bucket pair j = tid: prefix over warps; packed scan of
       // (tile count | complete chunks of carry + run) ----
       uint32_t s = 0, n0 = 0, n1 = 0, f0 = 0, f1 = 0;
       uint2 I0 = make_uint2(0, 0), I1 = make_uint2(0, 0);
-      const uint2* cin = cst + cs * (TL::NBW + 1);
+      const uint2* cin = cst;
       const uint32_t pj = tid / PT, pq = tid % PT;  // bucket pair, part of it
       const bool own = pj < npair;
       if (own) {
@@ -355,7 +359,7 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
         if (own) {
           const uint32_t t0 = ex & 0xffffu, c0 = ex >> 16;
           // next carry state and the copy that produces it
-          uint2* cout = cst + (cs ^ 1) * (TL::NBW + 1);
+          uint2* cout = cst;
           auto next = [&](uint32_t b, uint2 I, uint32_t n, uint32_t f, uint32_t t) {
             const uint32_t cc = I.x & 0xffffu;
             if (f == 0) {
@@ -373,13 +377,17 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
             for (uint32_t k = 0; k < f; ++k)
               cdesc[g0 + k] = make_uint2(I.y + k * C, (t - cc + k * C + 16u) | (k ? 0u : ((cc << 14) | (ch << 18))) | (b << 22));
           };
+          // the last staging slot of a bucket run (order check, repair)
+          auto mark_end = [&](uint32_t e) { atomicOr(&bend[e >> 5], 1u << (e & 31)); };
           if (pq == 0) {
             next(2 * pj, I0, n0, f0, t0);
             chunks(2 * pj, I0, f0, t0, c0);
+            if (n0) mark_end(t0 + n0 - 1);
           }
           if (pq == PT - 1 && 2 * pj + 1 < nb) {
             next(2 * pj + 1, I1, n1, f1, t0 + n0);
             chunks(2 * pj + 1, I1, f1, t0 + n0, c0 + f0);
+            if (n1) mark_end(t0 + n0 + n1 - 1);
           }
           // fold the tile offsets (and the earlier parts' counts) into this
           // part's per-warp prefixes
@@ -401,7 +409,7 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
           const uint32_t b = bk[i] >> 16;
           const uint32_t p = ((mywh[b >> 1] >> ((b & 1u) << 4)) & 0xffffu) + (bk[i] & 0xffffu);
           st_put(p, key[i], VB ? val[i] : V(0));
-          pk[p] = (b << 16) | (warp * WS + i * 32 + lane);
+          pk[p] = (uint16_t)(warp * WS + i * 32 + lane);
         }
       }
       __syncwarp();
@@ -434,9 +442,9 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       };
       {
         bool bad = false;
-        for (uint32_t p = tid; p < tn; p += NT) {
-          const uint32_t wd = pk[p], nx = pk[p + 1];
-          bad |= ((wd ^ nx) < 65536u) & (nx < wd);
+        for (uint32_t p = tid; p + 1 < tn; p += NT) {
+          const bool same = !((bend[p >> 5] >> (p & 31)) & 1u);
+          bad |= same & (pk[p + 1] < pk[p]);
         }
         if (__any_sync(FULL, bad) && lane == 0) s_fix = 1u;
       }
@@ -449,14 +457,14 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
 #endif
         // re-sort each bucket run by tile position (insertion sort), then
         // write the chunks again (same addresses, corrected values)
+        auto run_end = [&](uint32_t q) { return ((bend[q >> 5] >> (q & 31)) & 1u) != 0u; };
         for (uint32_t p = tid; p < tn; p += NT) {
-          const uint32_t x = pk[p];
-          const bool leader = p == 0 || ((pk[p - 1] ^ x) >= 65536u);
-          if (leader && p + 1 < tn && ((pk[p + 1] ^ x) < 65536u)) {
+          const bool leader = p == 0 || run_end(p - 1);
+          if (leader && p + 1 < tn && !run_end(p)) {
             uint32_t c = 2;
-            while (p + c < tn && ((pk[p + c] ^ x) < 65536u)) ++c;
+            while (p + c < tn && !run_end(p + c - 1)) ++c;
             for (uint32_t a = 1; a < c; ++a) {
-              const uint32_t xw = pk[p + a];
+              const uint16_t xw = pk[p + a];
               K xk2;
               V xv2 = V(0);
               st_get(p + a, xk2, xv2);
@@ -525,7 +533,7 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       for (uint32_t b0 = warp * BPW; b0 < nb; b0 += NW * BPW) {
         const uint32_t b = b0 + sub;
         if (b < nb) {
-          const uint2 I = cst[cs * (TL::NBW + 1) + b];
+          const uint2 I = cst[b];
           if (r >= (I.x >> 16) && r < (I.x & 0xffffu)) {
             st_global(ko_seg + I.y + r, ck[b * CP + r]);
             if (VB) st_global(vo_seg + I.y + r, cv[b * CP + r]);
