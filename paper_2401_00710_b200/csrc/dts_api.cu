@@ -56,7 +56,7 @@ constexpr int SAMPLE_NT = 1024;
 inline uint64_t scatter_T(int kb, int vb) { return (kb == 4 && vb <= 4) ? 512 * 9 : 512 * 5; }
 inline uint64_t block_records(int kb, int vb) { return scatter_T(kb, vb) * 8; }
 // write-combining scatter: stripe (= count-matrix row) of WC_LBS tiles
-constexpr uint64_t WC_LBS = 64;
+constexpr uint64_t WC_LBS = 44;  // ~315 K records (u32/u32 tiles of 7168): boundary cost vs last-wave imbalance
 constexpr uint32_t COPY_CHUNK = 1u << 16;
 // sample iff n' >= SAMPLE_FACTOR x |S|.  The reference samples from 2|S|
 // (dtsort.py:225); here small segments skip it: heavy keys found there save
