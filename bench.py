@@ -285,6 +285,7 @@ def run_ours(args, cfgd, rank, world, local_rank):
     clocks.start()
     total_ms = 0.0
     reps = []
+    dstats = []
     stream = torch.cuda.current_stream(dev)
     if multi:
         ops.launches = 0
@@ -301,6 +302,7 @@ def run_ours(args, cfgd, rank, world, local_rank):
         b.synchronize()
         total_ms += a.elapsed_time(b)
         reps.append(rep)
+        dstats.append(st)
     torch.cuda.synchronize()
     if multi:
         dist.barrier()
@@ -320,6 +322,25 @@ def run_ours(args, cfgd, rank, world, local_rank):
     peak, peak_kind = peaks()
     roof = None
     launches = int(ops.launches) if multi else None
+    if multi:
+        # SURVEY.md §8(d), G GPUs: per rank B_HBM = beta * (n_in (partition
+        # pass) + D_local), B_NVL = bytes sent to other ranks; T_roof = max over
+        # ranks of B_HBM / HBM peak + B_NVL / 900 GB/s (NVLink 5 per direction)
+        beta = kb + 2 * (kb + vb)
+        sts = [s for s in dstats if s is not None]
+        b_hbm = beta * (sum(s.n_local_in for s in sts) + sum(s.local_distributed for s in sts)) / max(len(sts), 1)
+        b_nvl = sum(s.bytes_sent_remote for s in sts) / max(len(sts), 1)
+        x_ms = sum(s.exchange_ms for s in sts) / max(len(sts), 1)
+        t = torch.tensor([b_hbm / (peak * 1e9) + b_nvl / 900e9, b_hbm, b_nvl, x_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_roof, hbm_max, nvl_max, xmax = [float(x) for x in t.tolist()]
+        roof = {"bound": "hbm+nvlink", "achieved": round(n_total / (ms / 1e3) / 1e9, 4), "unit": "Gkeys/s",
+                "frac": round(t_roof * 1e3 / ms, 4), "peak_hbm_GBps": peak, "peak_nvlink_GBps": 900.0,
+                "peak_kind": peak_kind, "traffic": None,
+                "B_hbm_GB_max_rank": round(hbm_max / 1e9, 3), "B_nvlink_GB_max_rank": round(nvl_max / 1e9, 3),
+                "T_roof_ms": round(t_roof * 1e3, 3),
+                "exchange_ms_max_rank": round(xmax, 3),
+                "exchange_GBps": round(nvl_max / (xmax / 1e3) / 1e9, 1) if xmax > 0 else None}
     if not multi and reps and reps[0] is not None:
         sc_ms = sum(r.kernel_ms["scatter"] for r in reps)
         sc_launch = sum(r.kernel_launches["scatter"] for r in reps)

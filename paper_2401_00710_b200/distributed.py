@@ -40,6 +40,8 @@ class DistStats:
     send_counts: list
     recv_counts: list
     bytes_sent_remote: int
+    exchange_ms: float = 0.0     # record all-to-all (keys + values), CUDA events on the caller's stream
+    local_distributed: int = 0   # records the local dts_sort distributed (its D)
 
 
 def choose_splitters(sample_keys: np.ndarray, sample_idx: np.ndarray, G: int):
@@ -190,13 +192,24 @@ def dist_sort(keys, vals=None, group=None, ops=None, samples_per_rank: int = 1 <
     recv = [int(x) for x in recv_t.cpu().tolist()]
     n_out = sum(recv)
     rk = ops.empty_like(pk, n_out)
+    timed = dev.type == "cuda"
+    if timed:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
     dist.all_to_all_single(_comm_view(rk), _comm_view(pk), recv, send, group=group)
     rv = None
     if vals is not None:
         rv = ops.empty_like(pv, n_out)
         dist.all_to_all_single(_comm_view(rv), _comm_view(pv), recv, send, group=group)
+    if timed:
+        e1.record()
     # 4. local stable sort of the received range
-    ops.sort(rk, rv)
+    rep = ops.sort(rk, rv)
     rec_bytes = keys.element_size() + (0 if vals is None else vals.element_size())
     remote = sum(send) - send[rank]
-    return rk, rv, DistStats(n_local, n_out, send, recv, remote * rec_bytes)
+    st = DistStats(n_local, n_out, send, recv, remote * rec_bytes)
+    if timed:
+        e1.synchronize()
+        st.exchange_ms = float(e0.elapsed_time(e1))
+    st.local_distributed = int(getattr(rep, "records_distributed", 0) or 0)
+    return rk, rv, st
