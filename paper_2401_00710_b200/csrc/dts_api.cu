@@ -324,7 +324,10 @@ struct Sorter {
   }
 
   void flush_span() {
-    if (have_cur && cur.len) spans.push_back(cur);
+    if (have_cur && cur.len) {
+      cur.src |= SPAN_NOBOUND << 8;  // (host spans: key bound unknown)
+      spans.push_back(cur);
+    }
     have_cur = false;
   }
   void add_span(uint64_t lo, uint64_t sz, uint32_t src) {

@@ -57,8 +57,11 @@ struct Blk {
 struct Span {
   uint64_t offset;
   uint32_t len;
-  uint32_t src;  // 0: records are in A (caller buffer), 1: in T (temporary)
+  // bit 0: records are in A (caller buffer, 0) or T (temporary, 1);
+  // bits 8-15: the keys agree above this bit (SPAN_NOBOUND: unknown)
+  uint32_t src;
 };
+constexpr uint32_t SPAN_NOBOUND = 255u;
 
 // A finished range that must be copied T -> A (dtsort.py:111-124).
 struct CopyR {

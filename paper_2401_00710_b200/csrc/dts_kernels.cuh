@@ -503,7 +503,9 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(const SegPlan* __restrict__
     for (uint32_t b = threadIdx.x; b < nb; b += CLS_NT) {
       if (s_ty[b] == T_CAND) {
         const uint32_t sz = (uint32_t)(s_bs[b + 1] - s_bs[b]);
-        s_sp[atomicAdd(&s_n[0], 1u)] = Span{P.offset + s_bs[b], sz, out_src};
+        // one light bucket: its keys agree on every bit from the digit up
+        const uint32_t bound = kinds[P.bs_base + b] == KIND_LIGHT ? P.shift : SPAN_NOBOUND;
+        s_sp[atomicAdd(&s_n[0], 1u)] = Span{P.offset + s_bs[b], sz, out_src | (bound << 8)};
         rec += sz;
       }
     }
@@ -520,11 +522,15 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(const SegPlan* __restrict__
         const uint64_t lo = P.offset + s_bs[b];
         const uint32_t sz = (uint32_t)(s_bs[b + 1] - s_bs[b]);
         spanrec += sz;
+        const uint32_t bound = kinds[P.bs_base + b] == KIND_LIGHT ? P.shift : SPAN_NOBOUND;
         if (have && cur.offset + cur.len == lo && cur.len + sz <= thr) {
-          cur.len += sz;
+          cur.len += sz;  // several buckets: the keys agree above the digit
+          const uint32_t cb = (cur.src >> 8) & 255u;
+          const uint32_t nbd = (cb == SPAN_NOBOUND || bound == SPAN_NOBOUND) ? SPAN_NOBOUND : P.shift + P.gamma;
+          cur.src = (cur.src & 255u) | (nbd << 8);
         } else {
           if (have) s_sp[nsp++] = cur;
-          cur = Span{lo, sz, out_src};
+          cur = Span{lo, sz, out_src | (bound << 8)};
           have = true;
         }
       } else {

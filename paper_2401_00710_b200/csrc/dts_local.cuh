@@ -86,8 +86,8 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
 
   // issue span `s` into buffer `b` (thread 0; the descriptor is in hand)
   auto issue = [&](const Span& S, int b) {
-    const K* kc = S.src ? Tk : Ak;
-    const V* vc = S.src ? Tv : Av;
+    const K* kc = (S.src & 1u) ? Tk : Ak;
+    const V* vc = (S.src & 1u) ? Tv : Av;
     SpanSlot sl;
     sl.offset = S.offset;
     sl.len = S.len;
@@ -144,39 +144,47 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
     V* ov = VB ? Av + S.offset : nullptr;
 
     // ---- keys into registers (lane-striped warp sub-tiles), differing bits ----
+    // (a span of one light bucket comes with its bound: the keys agree above
+    // it, so the counting path starts without a reduction or a barrier;
+    // otherwise the differing bits are reduced over the span)
     const K k0 = sk[0];
     K key[IPT];
     K diff = 0;
+    const uint32_t bound = (S.src >> 8) & 255u;
+    const bool known = bound <= (uint32_t)TL::NB;
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
       const uint32_t e = warp * WS + i * 32 + lane;
       key[i] = e < n ? sk[e] : k0;
       diff |= key[i] ^ k0;
     }
+    int bits = (int)bound;
+    if (!known) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) diff |= __shfl_xor_sync(FULL, diff, o);
-    if (lane == 0) s_diff[warp] = diff;
-    if (tid == 0) s_big = 0u;  // read only after the scan barrier below
-    __syncthreads();
+      for (int o = 16; o > 0; o >>= 1) diff |= __shfl_xor_sync(FULL, diff, o);
+      if (lane == 0) s_diff[warp] = diff;
+      __syncthreads();
+    }
     PH(1)
     // stream the next span into the other buffer (freed by the previous
-    // iteration's final barrier); fetch the descriptor after it.  Done by the
-    // last thread after the first barrier so no warp starts the span late.
+    // iteration's final barrier); fetch the descriptor after it
     if (tid == NT - 1) {
       if (sidx + G < nspan) issue(nextS, cur ^ 1);
       if (sidx + 2 * G < nspan) nextS = spans[sidx + 2 * G];
     }
-    diff = 0;
+    if (!known) {
+      diff = 0;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) diff |= s_diff[w];
-    int bits = 0;
-    if (diff) bits = (sizeof(K) == 8) ? 64 - __clzll((long long)diff) : 32 - __clz((int)(uint32_t)diff);
+      for (int w = 0; w < NW; ++w) diff |= s_diff[w];
+      bits = 0;
+      if (diff) bits = (sizeof(K) == 8) ? 64 - __clzll((long long)diff) : 32 - __clz((int)(uint32_t)diff);
+    }
 
     if (bits == 0) {
 #if DTS_PHASE_PROF == 2
       if (tid == 0) atomicAdd(&g_phase[15], 1ull);
 #endif
-      if (S.src) {
+      if (S.src & 1u) {
         for (uint32_t i = tid; i < n; i += NT) {
           ok[i] = sk[i];
           if (VB) ov[i] = sv[i];
@@ -359,6 +367,9 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
           ok[p] = hi | (K)(w >> 16);
           if (VB) ov[p] = sv[w & 0xffffu];
         }
+        // bins ready for the next span before E's barrier (the next span may
+        // start its atomics without a barrier of its own)
+        for (uint32_t q = tid; q < nq; q += NT) reinterpret_cast<uint4*>(cnt)[q] = make_uint4(0u, 0u, 0u, 0u);
         if (__syncthreads_or(bad) || DTS_FORCE_FIXUP) {
 #if DTS_PHASE_PROF == 2
           if (tid == 0) atomicAdd(&g_phase[12], 1ull);
@@ -387,10 +398,9 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
             ok[p] = hi | (K)(w >> 16);
             if (VB) ov[p] = sv[w & 0xffffu];
           }
+          __syncthreads();  // (the next span may reuse this buffer right away)
         }
         PH(7)
-        // ready for the next span (ordered before its atomics by its first barrier)
-        for (uint32_t q = tid; q < nq; q += NT) reinterpret_cast<uint4*>(cnt)[q] = make_uint4(0u, 0u, 0u, 0u);
         PH(8)
         continue;
       }
@@ -470,6 +480,31 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
 #if DTS_PHASE_PROF == 2
       if (tid == 0) atomicAdd(&g_phase[13], 1ull);
 #endif
+    if (known) {
+      // the span's bound is only an upper bound: the LSD passes follow the
+      // bits its keys really differ in (duplicate-heavy spans: often few)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) diff |= __shfl_xor_sync(FULL, diff, o);
+      if (lane == 0) s_diff[warp] = diff;
+      __syncthreads();
+      diff = 0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) diff |= s_diff[w];
+      bits = 0;
+      if (diff) bits = (sizeof(K) == 8) ? 64 - __clzll((long long)diff) : 32 - __clz((int)(uint32_t)diff);
+      if (bits == 0) {  // all keys equal: in place already, or one copy from T
+        if (S.src & 1u) {
+          for (uint32_t i = tid; i < n; i += NT) {
+            ok[i] = sk[i];
+            if (VB) ov[i] = sv[i];
+          }
+        }
+        for (uint32_t i = tid; i < (uint32_t)(SL::cnt_bytes / 4); i += NT) cnt[i] = 0u;
+        if (tid == 0) s_big = 0u;
+        __syncthreads();
+        continue;
+      }
+    }
     uint32_t idx[IPT];
 #pragma unroll
     for (int i = 0; i < IPT; ++i) idx[i] = warp * WS + i * 32 + lane;
@@ -574,6 +609,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
       if (VB) ov[p] = sv[si[p] & 0xffffu];
     }
     for (uint32_t i = tid; i < (uint32_t)(SL::cnt_bytes / 4); i += NT) cnt[i] = 0u;
+    if (tid == 0) s_big = 0u;  // (only the LSD path is entered with it set)
     __syncthreads();
   }
   PH_DONE
