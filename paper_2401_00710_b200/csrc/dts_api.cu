@@ -168,6 +168,18 @@ struct Timer {
     pending.push_back(ev);
   }
   void harvest() {  // call after a stream sync
+    // DTS_TIMELINE=1 (profiled runs): every timed launch as start/end in ms
+    // from the first one — the gaps between launches are host round trips
+    static const int tl = env_int("DTS_TIMELINE", 0);
+    if (tl && !pending.empty()) {
+      static const char* names[] = {"sample", "hist", "scan", "scatter", "local", "copy", "bounds", "merge"};
+      for (auto& e : pending) {
+        float a = 0.f, b = 0.f;
+        cudaEventElapsedTime(&a, pending[0].a, e.a);
+        cudaEventElapsedTime(&b, pending[0].a, e.b);
+        std::fprintf(stderr, "[dts-timeline] %-8s %9.3f %9.3f ms\n", names[e.cls], a, b);
+      }
+    }
     for (auto& e : pending) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, e.a, e.b);
