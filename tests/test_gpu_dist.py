@@ -36,6 +36,7 @@ for kb, n in ((4, 1_000_003), (8, 300_000)):
     rk, rv, st = dist_sort(tk, tv)
     ok = np.array_equal(rk.cpu().numpy().view(dt), wk) and np.array_equal(rv.cpu().numpy().view(dt), wv)
     assert ok and st.n_local_out == n and st.bytes_sent_remote == 0, (kb, n)
+    assert st.exchange_ms > 0.0 and st.local_distributed >= n, (st.exchange_ms, st.local_distributed)
 dist.destroy_process_group()
 print("ok")
 """
