@@ -103,6 +103,14 @@ class Clocks:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_first(self, timeout_s: float = 5.0):
+        """Block until nvidia-smi has produced its first sample (its start-up
+        can outlast a short timed region)."""
+        t0 = time.time()
+        while self.proc is not None and not self.lines and time.time() - t0 < timeout_s:
+            time.sleep(0.01)
+        self.lines.clear()  # keep only samples taken from here on
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -283,6 +291,7 @@ def run_ours(args, cfgd, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     clocks.start()
+    clocks.wait_first()
     total_ms = 0.0
     reps = []
     dstats = []
