@@ -52,15 +52,15 @@ CONFIGS = {
     "c2": dict(desc="C2 u32 key + u32 value, keys uniform [0,1e9), values = index, n=1e9",
                n=10**9, kb=4, vb=4, dist="uniform1e9"),
     "c3-zipf0.6": dict(desc="C3 Zipf s=0.6 ranks over 1..1e9 mapped by a seeded permutation",
-                       n=10**9, kb=4, vb=4, dist="zipf", s=0.6),
-    "c3-zipf1.0": dict(desc="C3 Zipf s=1.0", n=10**9, kb=4, vb=4, dist="zipf", s=1.0),
-    "c3-zipf1.2": dict(desc="C3 Zipf s=1.2", n=10**9, kb=4, vb=4, dist="zipf", s=1.2),
-    "c3-zipf1.5": dict(desc="C3 Zipf s=1.5", n=10**9, kb=4, vb=4, dist="zipf", s=1.5),
+                       n=10**9, kb=4, vb=4, dist="zipf", s=0.6, D_ref=2.9997e9),
+    "c3-zipf1.0": dict(desc="C3 Zipf s=1.0", n=10**9, kb=4, vb=4, dist="zipf", s=1.0, D_ref=2.3637e9),
+    "c3-zipf1.2": dict(desc="C3 Zipf s=1.2", n=10**9, kb=4, vb=4, dist="zipf", s=1.2, D_ref=1.4729e9),
+    "c3-zipf1.5": dict(desc="C3 Zipf s=1.5", n=10**9, kb=4, vb=4, dist="zipf", s=1.5, D_ref=1.1554e9),
     "c4-exp1e-5": dict(desc="C4 u64/u64 keys floor(Exp(rate 1e-5))", n=10**9, kb=8, vb=8,
-                       dist="exp", rate=1e-5),
+                       dist="exp", rate=1e-5, D_ref=3.5897e9),
     "c4-exp1e-7": dict(desc="C4 u64/u64 keys floor(Exp(rate 1e-7))", n=10**9, kb=8, vb=8,
-                       dist="exp", rate=1e-7),
-    "c4-bexp": dict(desc="C4 u64/u64 keys w >> Geometric(0.5)", n=10**9, kb=8, vb=8, dist="bexp"),
+                       dist="exp", rate=1e-7, D_ref=2.9198e9),
+    "c4-bexp": dict(desc="C4 u64/u64 keys w >> Geometric(0.5)", n=10**9, kb=8, vb=8, dist="bexp", D_ref=2.1875e9),
     # graph transpose: n is the TOTAL edge count, split over the ranks
     # (strong scaling); key = dst, value = src, both uint32
     "c5": dict(desc="C5 R-MAT 2^28 vertices, 2^32 edges (a,b,c,d)=(.57,.19,.19,.05), (dst, src) sorted "
@@ -377,7 +377,10 @@ def run_ours(args, cfgd, rank, world, local_rank):
                 "algorithmic_bytes_per_launch": int(per_launch_bytes),
                 "ms_per_launch": round(per_launch_ms, 4),
                 "step_share": shares}
-        D_ref = 3 * n if args.config == "c2" else None
+        # D of the reference's own distribution structure (SURVEY.md §8d
+        # table, wrapper-measured on these configs), scaled to --n
+        D_ref = 3 * n if args.config == "c2" else (
+            int(cfgd["D_ref"] * n / CONFIGS[args.config]["n"]) if "D_ref" in cfgd else None)
         D_ours = reps[0].records_distributed
         beta = kb + 2 * (kb + vb)
         pipe = {"beta_bytes": beta, "D_ours": D_ours, "D_reference": D_ref,
