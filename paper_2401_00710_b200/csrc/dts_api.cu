@@ -738,10 +738,10 @@ struct Sorter {
     meta.off = save;
     if (trace_on()) {
       std::fprintf(stderr,
-                   "[dts] level %d segs %zu recs %llu blks %zu tiles %llu sampled %zu wc %d | plan+launch %.0f us, "
+                   "[dts] level %d segs %zu recs %llu blks %zu tiles %llu sampled %zu wc %d nbc %u | plan+launch %.0f us, "
                    "wait %.0f us, spans %llu copies %llu next %llu, host %.0f us\n",
                    level, ns, (unsigned long long)wave_recs, blks.size(), (unsigned long long)ntile,
-                   sampled.size(), (int)wc, t_launch - t_plan0, t_sync - t_launch,
+                   sampled.size(), (int)wc, nbc, t_launch - t_plan0, t_sync - t_launch,
                    (unsigned long long)nsp, (unsigned long long)ncp, (unsigned long long)nnx,
                    now_us() - t_sync);
     }
