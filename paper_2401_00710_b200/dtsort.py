@@ -178,6 +178,7 @@ def _run(records: RecordArray, cfg: SortConfig | None, mode: int) -> InstrumentR
     with torch.cuda.device(device):
         kcol = Column(records.keys, device, None)
         vcol = Column(records.payloads, device, None) if records.payloads is not None else None
+        trace = _trace_sort(kcol.dev, cfg, mode) if cfg.instrument and n < split_n() else None
         rep = sort_device(kcol.dev, None if vcol is None else vcol.dev, cfg, mode)
         kcol.writeback()
         if vcol is not None:
@@ -185,4 +186,46 @@ def _run(records: RecordArray, cfg: SortConfig | None, mode: int) -> InstrumentR
         torch.cuda.current_stream(device).synchronize()
     if not cfg.instrument:
         return None
+    if trace is not None:
+        rep = _reference_report(rep, trace, cfg, mode)
+    return rep
+
+
+def _host_u(t):
+    """Device tensor of 4/8-byte elements -> numpy unsigned array (bit copy)."""
+    torch = torch_mod()
+    import numpy as np
+
+    if t.element_size() == 4:
+        return t.view(torch.int32).cpu().numpy().view(np.uint32)
+    return t.view(torch.int64).cpu().numpy().view(np.uint64)
+
+
+def _trace_sort(keys, cfg: SortConfig, mode: int):
+    """Instrument mode: the inputs of the counter replay (replay.py) — the
+    keys in input order, and the stable (keys, index) sort done by dts_sort
+    on the GPU before the caller's records are sorted."""
+    torch = torch_mod()
+    n = int(keys.numel())
+    keys_in = _host_u(keys)
+    ks = keys.clone()
+    idx = torch.arange(n, dtype=torch.int32 if n < 2**31 else torch.int64, device=keys.device)
+    sort_device(ks, idx, SortConfig(seed=cfg.seed), mode)
+    return keys_in, _host_u(ks), idx.cpu().numpy().astype("int64")
+
+
+def _reference_report(gpu: InstrumentReport, trace, cfg: SortConfig, mode: int) -> InstrumentReport:
+    """The reference's counters (replay.py); the GPU's own structure stays
+    available as ``rep.gpu`` and its timing / launch fields are carried over."""
+    from .replay import replay_report
+
+    keys_in, ks, perm = trace
+    rep = replay_report(keys_in, ks, perm, cfg, plain=mode == _lib.MODE_PLAIN)
+    rep.gpu = gpu
+    if gpu is not None:
+        rep.records_distributed = gpu.records_distributed
+        rep.gpu_launches = gpu.gpu_launches
+        rep.kernel_ms = gpu.kernel_ms
+        rep.kernel_launches = gpu.kernel_launches
+        rep.kernel_records = gpu.kernel_records
     return rep
