@@ -335,6 +335,45 @@ struct Sorter {
     return true;
   }
 
+  // The base case over a span list (count device-resident): k_local_sort,
+  // then the 8-bit-field retry (k_local_sort<.., true>) of the spans whose
+  // 4-bit counting pass would carry — duplicate-rich spans, queued on the
+  // device by the first launch — so the common path's code stays as it is.
+  int local_sort_launch(const Span* dsp, const uint32_t* dn, uint64_t cap, uint32_t grid_hint, uint64_t recs) {
+    static const int retry = env_int("DTS_LOCAL_RETRY", 1);
+    constexpr int NT = LocalTile<K, VB>::NT;
+    const size_t sm = LocalSmem<K, VB>::total;
+    Span* rq = nullptr;
+    uint32_t* rqn = nullptr;
+    if (retry) {
+      rq = (Span*)meta.take(std::max<uint64_t>(1, cap) * sizeof(Span));
+      rqn = (uint32_t*)meta.take(16);
+      if (!rq || !rqn) return fail(DTS_ENOMEM, "workspace too small for the local-sort retry queue");
+      CUDA_TRY(cudaMemsetAsync(rqn, 0, 4, st));
+    }
+    {
+      Timer::Ev ev;
+      tm.begin(DTS_K_LOCAL, ev);
+      auto fn = k_local_sort<K, VB, false>;
+      DTS_TRY(set_smem(fn, sm));
+      const int grid = persistent_grid(fn, NT, sm, grid_hint);
+      fn<<<grid, NT, sm, st>>>(dsp, dn, Ak, Av, Tk, Tv, rq, rqn);
+      tm.end(ev, recs);
+      DTS_TRY(check_launch("k_local_sort"));
+    }
+    if (retry) {
+      Timer::Ev ev;
+      tm.begin(DTS_K_LOCAL, ev);
+      auto fr = k_local_sort<K, VB, true>;
+      DTS_TRY(set_smem(fr, sm));
+      const int grid = persistent_grid(fr, NT, sm, grid_hint);
+      fr<<<grid, NT, sm, st>>>(rq, rqn, Ak, Av, Tk, Tv, nullptr, nullptr);
+      tm.end(ev, 0);
+      DTS_TRY(check_launch("k_local_sort (retry)"));
+    }
+    return 0;
+  }
+
   void flush_span() {
     if (have_cur && cur.len) {
       cur.src |= SPAN_NOBOUND << 8;  // (host spans: key bound unknown)
@@ -385,15 +424,7 @@ struct Sorter {
     uint64_t recs = 0;
     for (const Span& x : spans) recs += x.len;
     if (!spans.empty()) {
-      Timer::Ev ev;
-      tm.begin(DTS_K_LOCAL, ev);
-      auto fn = k_local_sort<K, VB>;
-      const size_t sm = LocalSmem<K, VB>::total;
-      DTS_TRY(set_smem(fn, sm));
-      const int grid = persistent_grid(fn, LocalTile<K, VB>::NT, sm, (uint32_t)spans.size());
-      fn<<<grid, LocalTile<K, VB>::NT, sm, st>>>(dsp, dcnt, Ak, Av, Tk, Tv);
-      tm.end(ev, recs);
-      DTS_TRY(check_launch("k_local_sort"));
+      DTS_TRY(local_sort_launch(dsp, dcnt, spans.size(), (uint32_t)spans.size(), recs));
       if (rep) {
         rep->base_case_records += recs;
         rep->moves += recs;
@@ -688,17 +719,7 @@ struct Sorter {
       tm.end(ev, wave_recs);
       DTS_TRY(check_launch("k_scatter"));
     }
-    {
-      Timer::Ev ev;
-      tm.begin(DTS_K_LOCAL, ev);
-      auto fn = k_local_sort<K, VB>;
-      const size_t sm = LocalSmem<K, VB>::total;
-      DTS_TRY(set_smem(fn, sm));
-      const int grid = persistent_grid(fn, LocalTile<K, VB>::NT, sm, 1u << 30);
-      fn<<<grid, LocalTile<K, VB>::NT, sm, st>>>(dspan, reinterpret_cast<const uint32_t*>(dcc), Ak, Av, Tk, Tv);
-      tm.end(ev, 0);
-      DTS_TRY(check_launch("k_local_sort"));
-    }
+    DTS_TRY(local_sort_launch(dspan, reinterpret_cast<const uint32_t*>(dcc), bs_total, 1u << 30, 0));
     if (out_src == 1) {
       Timer::Ev ev;
       tm.begin(DTS_K_COPY, ev);

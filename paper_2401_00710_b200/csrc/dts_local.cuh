@@ -9,6 +9,14 @@ namespace dts {
 #define DTS_LOCAL_REGATOM 1  // register-sourced rank atomics (order verified on the output)
 #endif
 
+#ifndef DTS_OVN_LSD
+#define DTS_OVN_LSD 16 // wrapped 4-bit fields in one warp that send a span to LSD, not the retry
+#endif
+
+template <int FB> struct FieldBits {
+  static constexpr uint32_t value = FB;
+};
+
 template <typename K, int VB> struct LocalTile {
   // 8 warps: one 4-bit per-warp field per bin in a 32-bit bin word (the
   // stable counting path below); 2 CTAs per SM
@@ -62,11 +70,12 @@ struct SpanSlot {  // a span staged in one buffer
 //     (the k_scatter ranking; in-step order verified and repaired if needed).
 // Output always lands in A.
 // ---------------------------------------------------------------------------
-template <typename K, int VB>
+template <typename K, int VB, bool RETRY = false>
 __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
     k_local_sort(const Span* __restrict__ spans, const uint32_t* __restrict__ nspan_p, K* __restrict__ Ak,
                  typename ValOf<VB>::T* __restrict__ Av, const K* __restrict__ Tk,
-                 const typename ValOf<VB>::T* __restrict__ Tv) {
+                 const typename ValOf<VB>::T* __restrict__ Tv, Span* __restrict__ rq = nullptr,
+                 uint32_t* __restrict__ rq_n = nullptr) {
   using V = typename ValOf<VB>::T;
   using TL = LocalTile<K, VB>;
   using SL = LocalSmem<K, VB>;
@@ -81,7 +90,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
   __shared__ SpanSlot s_slot[2];
   __shared__ uint32_t s_wt[NW + 1];
   __shared__ K s_diff[NW];
-  __shared__ uint32_t s_fix, s_big;
+  __shared__ uint32_t s_fix, s_big, s_ovn;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   // issue span `s` into buffer `b` (thread 0; the descriptor is in hand)
@@ -114,6 +123,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
     fence_mbar_init();
     s_fix = 0u;
     s_big = 0u;
+    s_ovn = 0u;
   }
   __syncthreads();
   if (tid == NT - 1) {
@@ -249,49 +259,83 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
       for (uint32_t q = tid; q < nq; q += NT) reinterpret_cast<uint4*>(cnt)[q] = make_uint4(0u, 0u, 0u, 0u);
     };
     if (bits <= TL::NB) {
-      // ================= nibble counting path: the differing bits are the
+      // ================= field counting path: the differing bits are the
       // whole key order, so ONE stable counting pass sorts the span.  Bin
-      // word d holds a 4-bit count per warp (warp w at bits 4w), so a
-      // record's stable slot = start(d) + records of d in earlier warps
-      // (from the final word) + its own warp's earlier records of d (the
-      // atomic's return; the lane/instruction order of one warp's atomics is
-      // verified on the output).  Slot words hold (bin << 16 | position):
-      // the key is rebuilt from the bin, only the value is gathered.
+      // word d holds one FB-bit count per rank group — FB = 4: 8 groups, one
+      // per warp; FB = 8 (the retry launch): 4 groups, one per warp pair
+      // whose atomics run in two phases (even warps, then odd), so each
+      // group's counts still follow record order.  A record's stable slot =
+      // start(d) + records of d in earlier groups (from the final word) + its
+      // own group's earlier records of d (the atomic's return; the
+      // lane/instruction order of one warp's atomics is verified on the
+      // output).  Slot words hold (bin << 16 | position): the key is rebuilt
+      // from the bin, only the value is gathered.
       const uint32_t nbin = 1u << bits, mask = nbin - 1u, nq = (nbin + 3) >> 2;
       uint16_t* st16 = reinterpret_cast<uint16_t*>(smem_raw + (cur ? SL::k1 : SL::k0));  // bin starts
-      const uint32_t nib = 4u * (uint32_t)warp;
-      uint32_t rkp[(IPT + 7) / 8];  // own-warp ranks, 4 bits each
+      auto counting = [&](auto fbc) -> bool {
+        constexpr uint32_t FB = decltype(fbc)::value;
+        constexpr uint32_t FM = (1u << FB) - 1u;
+        constexpr int RPW = 32 / (int)FB;  // ranks per register word
+        auto fsum = [](uint32_t x) -> uint32_t {  // sum of the word's fields
+          if constexpr (FB == 4) {
+            x = (x & 0x0F0F0F0Fu) + ((x >> 4) & 0x0F0F0F0Fu);
+            return (x * 0x01010101u) >> 24;
+          } else {
+            return __dp4a(x, 0x01010101u, 0u);
+          }
+        };
+        const uint32_t nib = FB == 4 ? 4u * (uint32_t)warp : 8u * ((uint32_t)warp >> 1);
+        uint32_t rkp[(IPT + RPW - 1) / RPW];  // own-group ranks, FB bits each
 #pragma unroll
-      for (int j = 0; j < (IPT + 7) / 8; ++j) rkp[j] = 0u;
-      bool ovf = false;
-      // (the bins are zero here: zeroed at start and after every span)
-      PH(2)
-#if DTS_PHASE_PROF == 2
-      if (tid == 0) atomicAdd(&g_phase[11], 1ull);
-#endif
+        for (int j = 0; j < (IPT + RPW - 1) / RPW; ++j) rkp[j] = 0u;
+        bool ovf = false;
+        // (the bins are zero here: zeroed at start and after every span)
+        PH(2)
+        auto atomics = [&]() {
 #pragma unroll
-      for (int i = 0; i < IPT; ++i) {
-        const uint32_t e = warp * WS + i * 32 + lane;
-        if (e < n) {
+          for (int i = 0; i < IPT; ++i) {
+            const uint32_t e = warp * WS + i * 32 + lane;
+            if (e < n) {
 #if DTS_LOCAL_REGATOM
-          const uint32_t d = (uint32_t)key[i] & mask;
+              const uint32_t d = (uint32_t)key[i] & mask;
 #else
-          const uint32_t d = (uint32_t)sk[e] & mask;  // key read right before its atomic
+              const uint32_t d = (uint32_t)sk[e] & mask;  // key read right before its atomic
 #endif
-          const uint32_t r = (atomicAdd(&cnt[d], 1u << nib) >> nib) & 15u;
-          ovf |= r == 15u;
-          rkp[i >> 3] |= r << ((i & 7) * 4);
-        }
+              const uint32_t r = (atomicAdd(&cnt[d], 1u << nib) >> nib) & FM;
+              ovf |= r == FM;
+              rkp[i / RPW] |= r << ((i % RPW) * FB);
+            }
 #if !DTS_LOCAL_REGATOM
-        __syncwarp();
+            __syncwarp();
 #endif
-      }
-      if (ovf) s_big = 1u;  // a warp field would carry: LSD path
-      __syncthreads();
-      PH(3)
-      lsd = s_big != 0u;
-      if (!lsd) {
-        // exclusive scan of the bin totals (sum of the 8 fields) -> st16
+          }
+        };
+        if constexpr (FB == 4) {
+          atomics();
+        } else {
+          if (!(warp & 1)) atomics();
+          __syncthreads();
+          if (warp & 1) atomics();
+        }
+        if (ovf) s_big = 1u;  // a field would carry
+        __syncthreads();
+        PH(3)
+        if (s_big) {
+          if constexpr (FB == 4) {
+            // fields that wrapped in this warp (ranks of 15): many mean a
+            // key too frequent for 8-bit fields as well -> LSD directly
+            uint32_t ev = 0;
+#pragma unroll
+            for (int j = 0; j < (IPT + RPW - 1) / RPW; ++j) {
+              const uint32_t x = rkp[j];
+              ev += __popc(x & (x >> 1) & (x >> 2) & (x >> 3) & 0x11111111u);
+            }
+            ev = __reduce_add_sync(FULL, ev);
+            if (lane == 0) atomicMax(&s_ovn, ev);
+          }
+          return false;
+        }
+        // exclusive scan of the bin totals (sum of the fields) -> st16
         {
           // (<= 2^NB bins: at most QPT quads of 4 bin words per thread, kept
           // in registers across the barrier)
@@ -299,17 +343,13 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
           const uint32_t qpt = (nq + NT - 1) / NT;
           const uint32_t q0 = min(nq, tid * qpt), q1 = min(nq, q0 + qpt);
           const uint4* cq = reinterpret_cast<const uint4*>(cnt);
-          auto tot = [](uint32_t x) {
-            x = (x & 0x0F0F0F0Fu) + ((x >> 4) & 0x0F0F0F0Fu);
-            return (x * 0x01010101u) >> 24;
-          };
           uint4 xq[QPT];
 #pragma unroll
           for (uint32_t j = 0; j < QPT; ++j) xq[j] = q0 + j < q1 ? cq[q0 + j] : make_uint4(0u, 0u, 0u, 0u);
           uint32_t sum = 0;
 #pragma unroll
           for (uint32_t j = 0; j < QPT; ++j) {
-            xq[j] = make_uint4(tot(xq[j].x), tot(xq[j].y), tot(xq[j].z), tot(xq[j].w));
+            xq[j] = make_uint4(fsum(xq[j].x), fsum(xq[j].y), fsum(xq[j].z), fsum(xq[j].w));
             sum += xq[j].x + xq[j].y + xq[j].z + xq[j].w;
           }
           uint32_t incl = sum;
@@ -339,16 +379,14 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
         __syncthreads();
         PH(5)
         // slots
-        const uint32_t lowm = (1u << nib) - 1u;  // fields of earlier warps
+        const uint32_t lowm = (1u << nib) - 1u;  // fields of earlier groups
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
           const uint32_t e = warp * WS + i * 32 + lane;
           if (e < n) {
             const uint32_t d = (uint32_t)key[i] & mask;
-            uint32_t x = cnt[d] & lowm;
-            x = (x & 0x0F0F0F0Fu) + ((x >> 4) & 0x0F0F0F0Fu);
-            const uint32_t pre = (x * 0x01010101u) >> 24;
-            const uint32_t p = (uint32_t)st16[d] + pre + ((rkp[i >> 3] >> ((i & 7) * 4)) & 15u);
+            const uint32_t pre = fsum(cnt[d] & lowm);
+            const uint32_t p = (uint32_t)st16[d] + pre + ((rkp[i / RPW] >> ((i % RPW) * FB)) & FM);
             si[p] = (d << 16) | e;
           }
         }
@@ -402,8 +440,43 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
         }
         PH(7)
         PH(8)
-        continue;
+        return true;
+      };
+#if DTS_PHASE_PROF == 2
+      if (tid == 0) atomicAdd(&g_phase[11], 1ull);
+#endif
+      if constexpr (RETRY) {
+        if (counting(FieldBits<8>{})) continue;
+      } else {
+        if (counting(FieldBits<4>{})) continue;
+        if (rq != nullptr) {
+          // a 4-bit field would have carried: hand the span to the retry
+          // launch (8-bit fields) untouched; bins back to zero for the next
+          // span (every thread has read s_big before the reset)
+          for (uint32_t q = tid; q < nq; q += NT) reinterpret_cast<uint4*>(cnt)[q] = make_uint4(0u, 0u, 0u, 0u);
+          __syncthreads();
+          const uint32_t ovn = s_ovn;
+          __syncthreads();
+          const bool queue = ovn < (uint32_t)DTS_OVN_LSD;
+          if (tid == 0) {
+            s_ovn = 0u;
+            if (queue) {
+              s_big = 0u;
+              const uint32_t qi = atomicAdd(rq_n, 1u);
+              Span R;
+              R.offset = S.offset;
+              R.len = S.len;
+              R.src = S.src;
+              rq[qi] = R;
+            }
+          }
+          if (queue) {
+            __syncthreads();
+            continue;
+          }
+        }
       }
+      lsd = true;
     } else {
       // ================= counting path on the top CB of more differing bits;
       // records sharing those bits are ranked by (key, position) ======
