@@ -1,0 +1,55 @@
+"""Parity at BASELINE.json's full sizes (10^9 records) through the O(n)
+stable-sort certificate: with values = original index,
+the output is THE stable sort iff
+  1. keys are non-decreasing,
+  2. values are a permutation of 0..n-1,
+  3. values ascend inside every run of equal keys,
+  4. out_keys[i] == in_keys[out_vals[i]].
+This is the logic of the reference CLI's `verify` (bench.py:309-335); the
+oracle is too slow for 10^9 records, so the byte comparison against it runs
+at the sizes of tests/test_gpu_sort.py.  Chunked on the device so no
+n-sized int64 temporaries are needed beyond the gather."""
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = ["c2", "c3-zipf0.6", "c3-zipf1.0", "c3-zipf1.2", "c3-zipf1.5", "c4-exp1e-5", "c4-exp1e-7", "c4-bexp"]
+
+
+def _u(t):
+    import torch
+
+    return t.to(torch.int64) & 0xFFFFFFFF if t.element_size() == 4 else t
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_gpu_full_size_certificate(name):
+    import torch
+
+    import bench
+    from paper_2401_00710_b200 import SortConfig
+    from paper_2401_00710_b200.dtsort import sort_device
+
+    cfg = dict(bench.CONFIGS[name])
+    n = cfg["n"]
+    dev = torch.device("cuda", 0)
+    k, v = bench.gen_device(cfg, n, 7, dev)
+    k_in = k.clone()
+    sort_device(k, v, SortConfig(seed=7), 0)
+    torch.cuda.synchronize()
+    unsigned64 = k.element_size() == 8
+    CH = 1 << 27
+    seen = torch.zeros(n, dtype=torch.bool, device=dev)
+    for c0 in range(0, n, CH):
+        c1 = min(n, c0 + CH + 1)
+        kk, vv = _u(k[c0:c1]), _u(v[c0:c1])
+        if unsigned64:  # compare as unsigned: flip the sign bit
+            kk = kk ^ (-(2**63))
+        same = kk[1:] == kk[:-1]
+        assert bool((kk[1:] >= kk[:-1]).all()), f"{name}: keys not sorted near {c0}"
+        assert bool((~same | (vv[1:] > vv[:-1])).all()), f"{name}: equal keys out of input order near {c0}"
+        body = vv[: min(CH, n - c0)]
+        assert bool(((body >= 0) & (body < n)).all()), f"{name}: value out of range near {c0}"
+        seen[body] = True
+        assert bool((k[c0:c0 + body.numel()] == k_in[body]).all()), f"{name}: key/value pairing broken near {c0}"
+    assert bool(seen.all()), f"{name}: values are not a permutation of 0..n-1"
