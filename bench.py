@@ -485,6 +485,73 @@ def run_ours(args, cfgd, rank, world, local_rank):
         print(json.dumps(line), flush=True)
 
 
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """Re-exec this script as N torchrun ranks (one process per GPU).  Aborts
+    when fewer than N GPUs are visible (a run on fewer GPUs would print a
+    line for the wrong N)."""
+    if args.impl == "ours" and not args.gloo_selftest:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}",
+                  file=sys.stderr)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)]
+    # (torchrun's own parser would claim options such as --n: the ranks read
+    # this script's arguments from the environment instead)
+    env = dict(os.environ, DTS_BENCH_ARGV=json.dumps(sys.argv[1:]))
+    return subprocess.call(cmd, env=env)
+
+
+def run_gloo_selftest(args, cfgd, rank, world):
+    """CPU check of the multi-rank launch (tests/test_bench_launch.py): the
+    ranks join a gloo group, run distributed.dist_sort on a small seeded
+    input through a host ops double, take the max over ranks of the step
+    time and rank 0 prints the bench line shape with n_gpus = world."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2401_00710_b200.distributed import dist_sort
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from dist_hostops import HostOps  # test double: no GPU in a gloo self-test
+
+    dist.init_process_group("gloo")
+    try:
+        n = args.n or 4096
+        rng = np.random.default_rng(1000 + rank)
+        keys = torch.from_numpy(rng.integers(0, 10**9, size=n, dtype=np.uint32).view(np.int32))
+        vals = torch.arange(rank * n, (rank + 1) * n, dtype=torch.int32)
+        dist.barrier()
+        t0 = time.perf_counter()
+        rk, rv, st = dist_sort(keys, vals, ops=HostOps(), samples_per_rank=256)
+        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        got = torch.tensor([rk.numel()], dtype=torch.int64)
+        dist.all_reduce(got)
+        ok = bool((rk.to(torch.int64) & 0xFFFFFFFF).diff().ge(0).all()) if rk.numel() > 1 else True
+        okt = torch.tensor([int(ok)], dtype=torch.int64)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": round(n * world / float(t) / 1e9, 6),
+                              "unit": UNIT, "n_gpus": world, "steps": 1, "warmup": 0,
+                              "ms_per_step": round(float(t) * 1e3, 3), "selftest": "gloo",
+                              "records_out": int(got), "sorted": bool(okt.item())}), flush=True)
+    finally:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -499,13 +566,25 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU path (dist_sort) even at world size 1 (testing)")
-    args = ap.parse_args()
+    ap.add_argument("--gloo-selftest", action="store_true",
+                    help="CPU test of the multi-rank launch (gloo, host ops double; no GPU)")
+    argv = json.loads(os.environ["DTS_BENCH_ARGV"]) if "DTS_BENCH_ARGV" in os.environ else None
+    args = ap.parse_args(argv)
     cfgd = dict(CONFIGS[args.config])
     if args.n:
         cfgd["n"] = args.n
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N` outside torchrun: launch N ranks (one per
+        # GPU) under torch.distributed.run on 127.0.0.1 and relay rank 0's line
+        sys.exit(self_launch(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "ours" and world != args.gpus and not args.gloo_selftest:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.gloo_selftest:
+        run_gloo_selftest(args, cfgd, rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, cfgd, rank, world)
         return

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define DTS_ABI_VERSION 1
+#define DTS_ABI_VERSION 2
 
 #define DTS_OK 0
 #define DTS_EINVAL (-1)
@@ -95,22 +95,32 @@ int dts_sort(void* keys, void* vals, uint64_t n, int key_bytes, int val_bytes,
 /* Dovetail merge of one zone in place — replaces dt_merge (dtmerge.py:132-238).
  * zone = [sorted light run of light_len | heavy run 0 | heavy run 1 | ...].
  * heavy_keys (host, m keys, strictly increasing) / heavy_lens (host, m int64).
- * scratch must hold at least min(light_len, sum(heavy_lens)) records.
- * stats_out[3] = {out_copies, in_array_moves, restore_copies} (MergeStats).
- * validate != 0 runs the reference's _validate checks (dtmerge.py:108-129). */
+ * scratch_len must be at least min(light_len, sum(heavy_lens)) records (the
+ * reference's contract, checked with its messages); the GPU permutes the zone
+ * out of place through `workspace` (caller-owned device memory of at least
+ * dts_merge_workspace_bytes(zone_len, m, ...) bytes), so scratch is not
+ * written.  stats_out[3] = {out_copies, in_array_moves, restore_copies}: the
+ * reference's MergeStats for this zone.  validate != 0 runs the reference's
+ * _validate checks (dtmerge.py:108-129); on a validation error the zone is
+ * left unchanged.  Blocks once (reads the insertion points back). */
+size_t dts_merge_workspace_bytes(uint64_t zone_len, uint64_t m, int key_bytes,
+                                 int val_bytes);
 int dts_merge(void* zone_keys, void* zone_vals, uint64_t zone_len,
               uint64_t light_len, const void* heavy_keys,
               const int64_t* heavy_lens, uint64_t m, void* scratch_keys,
               void* scratch_vals, uint64_t scratch_len, int key_bytes,
-              int val_bytes, int validate, uint64_t stats_out[3], void* stream);
+              int val_bytes, int validate, void* workspace,
+              size_t workspace_bytes, uint64_t stats_out[3], void* stream);
 
 /* Stable G-way partition by (key, global index) against nsplit = G-1 sorted
  * splitters (host arrays split_keys / split_idx).  Record i (global index
  * global_base + i) goes to destination g = #{s : (split_key[s], split_idx[s])
  * < (key, global index)}.  Writes the records grouped by g (input order kept
  * within each group) to out_keys/out_vals and the group sizes to
- * send_counts[G] (host).  No reference counterpart (multi-GPU extension,
- * SURVEY.md §8e); built from the counting_sort machinery (counting.py:82-156). */
+ * send_counts[G] (host).  0 <= nsplit <= 1023 (G <= 1024: the splitter and
+ * bucket tables live in shared memory); larger nsplit returns DTS_EINVAL.
+ * No reference counterpart (multi-GPU extension); built from
+ * the counting_sort machinery (counting.py:82-156). */
 int dts_partition(const void* keys, const void* vals, uint64_t n,
                   uint64_t global_base, const void* split_keys,
                   const uint64_t* split_idx, int nsplit, void* out_keys,

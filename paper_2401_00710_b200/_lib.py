@@ -88,10 +88,11 @@ SIGNATURES = (
         [
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p,
             ctypes.POINTER(ctypes.c_int64), ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
-            ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+            ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
             ctypes.POINTER(ctypes.c_uint64), ctypes.c_void_p,
         ],
     ),
+    ("dts_merge_workspace_bytes", ctypes.c_size_t, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int]),
     (
         "dts_partition",
         ctypes.c_int,

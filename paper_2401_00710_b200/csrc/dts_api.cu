@@ -998,20 +998,72 @@ int partition_impl(const void* keys, const void* vals, uint64_t n, uint64_t gbas
 }
 
 // ---------------------------------------------------------------------------
-// Dovetail merge (dtmerge.py:132-238): layout on the GPU, the reference's
-// piece loop on the host, every move / reversal a grid-parallel kernel.
+// Dovetail merge (dtmerge.py:132-238) as a layout-driven permutation: the
+// insertion points (compute_layout, :58-78) and the reference's _validate
+// checks (:108-129) on the GPU, then one out-of-place pass of the zone into
+// the caller's workspace and one copy back — 3-4 launches and one read-back
+// of the insertion points, whatever the number of heavy runs.  MergeStats
+// are the reference's piece-loop counts, computed on the host from the
+// insertion points and run lengths (merge_stats below).
 // ---------------------------------------------------------------------------
+
+// The reference's write counts for a zone (dtmerge.py:166-238: out_copies of
+// the smaller side, in-array moves — a direct move of len, or a two-flip
+// block shift of 2 len (shift_block, :81-105) when source and destination
+// overlap — and restore copies from scratch).
+void merge_stats(uint64_t light, const int64_t* hlens, uint64_t m, const uint64_t* ins,
+                 const uint64_t* prefix, uint64_t heavy_total, uint64_t stats[3]) {
+  uint64_t out_copies = 0, in_moves = 0, restores = 0;
+  auto bound = [&](uint64_t i) -> uint64_t { return i == 0 ? 0 : (i <= m ? ins[i - 1] : light); };
+  if (heavy_total >= light) {
+    out_copies = light;
+    for (uint64_t i = 0; i < m; ++i) {
+      const uint64_t ln = (uint64_t)hlens[i], src = light + prefix[i], dst = ins[i] + prefix[i];
+      if (ln == 0 || dst == src) continue;
+      in_moves += dst + ln <= src ? ln : 2 * ln;
+    }
+    for (uint64_t i = 0; i <= m; ++i) {
+      const uint64_t f0 = bound(i), flen = bound(i + 1) - f0;
+      if (flen == 0 || f0 + prefix[i] == f0) continue;
+      restores += flen;
+    }
+  } else {
+    out_copies = heavy_total;
+    for (uint64_t i = m; i >= 1; --i) {
+      const uint64_t f0 = bound(i), flen = bound(i + 1) - f0, dst = f0 + prefix[i];
+      if (flen == 0 || dst == f0) continue;
+      in_moves += f0 + flen <= dst ? flen : 2 * flen;
+    }
+    for (uint64_t i = 0; i < m; ++i) restores += (uint64_t)hlens[i];
+  }
+  stats[0] = out_copies;
+  stats[1] = in_moves;
+  stats[2] = restores;
+}
+
+struct MergeWs {  // the caller's merge workspace, carved
+  size_t keys, vals, hk, pre, ins, err, total;
+};
+MergeWs merge_ws_layout(uint64_t zone_len, uint64_t m, int kb, int vb) {
+  MergeWs w;
+  w.keys = 0;
+  w.vals = align256(zone_len * (size_t)kb);
+  w.hk = w.vals + align256(zone_len * (size_t)vb);
+  w.pre = w.hk + align256(std::max<uint64_t>(1, m) * (size_t)kb);
+  w.ins = w.pre + align256((m + 1) * 8);
+  w.err = w.ins + align256(std::max<uint64_t>(1, m) * 8);
+  w.total = w.err + 256;
+  return w;
+}
+
 template <typename K, int VB>
 int merge_impl(void* zk_, void* zv_, uint64_t total, uint64_t light, const void* hkeys_,
-               const int64_t* hlens, uint64_t m, void* sk_, void* sv_, uint64_t scratch_len,
-               int validate, uint64_t stats[3], cudaStream_t st) {
+               const int64_t* hlens, uint64_t m, uint64_t scratch_len, bool scratch_vals, int validate,
+               void* ws_, size_t wsb, uint64_t stats[3], cudaStream_t st) {
   using V = typename ValOf<VB>::T;
   K* zk = (K*)zk_;
-  V* zv = (V*)zv_;
-  K* sk = (K*)sk_;
-  V* sv = (V*)sv_;
+  V* zv = VB ? (V*)zv_ : nullptr;
   const K* hkeys = (const K*)hkeys_;
-  const bool has_pay = VB != 0 && zv != nullptr;
   stats[0] = stats[1] = stats[2] = 0;
   int64_t heavy_total_s = 0;
   for (uint64_t i = 0; i < m; ++i) heavy_total_s += hlens[i];
@@ -1020,7 +1072,7 @@ int merge_impl(void* zk_, void* zv_, uint64_t total, uint64_t light, const void*
   if (scratch_len < small)
     return fail(DTS_EINVAL, "scratch holds " + std::to_string(scratch_len) + " records, need " +
                                 std::to_string(small));
-  if (has_pay && sv == nullptr && small > 0) return fail(DTS_EINVAL, "scratch payloads too small");
+  if (VB && zv && !scratch_vals && small > 0) return fail(DTS_EINVAL, "scratch payloads too small");
   if (validate) {
     if ((int64_t)light + heavy_total_s != (int64_t)total)
       return fail(DTS_EINVAL, "light_len plus heavy run lengths must tile the zone");
@@ -1035,145 +1087,65 @@ int merge_impl(void* zk_, void* zv_, uint64_t total, uint64_t light, const void*
     if (light + heavy_total != total)
       return fail(DTS_EINVAL, "light_len plus heavy run lengths must tile the zone");
   }
-  if (m == 0 || total == 0) {
-    if (validate && light > 1) {
-      // still validate light sortedness (dtmerge.py:119-121)
-    } else {
-      return 0;
-    }
-  }
+  const bool check_light = validate && light > 1;
+  if ((m == 0 || total == 0) && !check_light) return 0;
+  const MergeWs L = merge_ws_layout(total, m, sizeof(K), VB);
+  if (!ws_ || wsb < L.total)
+    return fail(DTS_ENOMEM, "merge workspace holds " + std::to_string(wsb) + " bytes, need " +
+                                std::to_string(L.total) + " (dts_merge_workspace_bytes)");
+  char* ws = (char*)ws_;
+  K* ok = (K*)(ws + L.keys);
+  V* ov = VB ? (V*)(ws + L.vals) : nullptr;
+  K* dh = (K*)(ws + L.hk);
+  uint64_t* dpre = (uint64_t*)(ws + L.pre);
+  uint64_t* dins = (uint64_t*)(ws + L.ins);
+  uint32_t* derr = (uint32_t*)(ws + L.err);
+  // heavy keys + run prefix sums up, through the pinned staging
   std::vector<uint64_t> prefix(m + 1, 0);
   for (uint64_t i = 0; i < m; ++i) prefix[i + 1] = prefix[i] + (uint64_t)hlens[i];
-  std::vector<uint64_t> p(m, 0);
-  K* dh = nullptr;
-  uint64_t* dtmp = nullptr;
-  uint32_t* derr = nullptr;
-  const size_t hbytes = std::max<uint64_t>(1, m) * sizeof(K);
-  const size_t tbytes = (2 * std::max<uint64_t>(1, m) + 2) * 8;
-  CUDA_TRY(cudaMallocAsync((void**)&dh, hbytes, st));
-  CUDA_TRY(cudaMallocAsync((void**)&dtmp, tbytes, st));
-  CUDA_TRY(cudaMallocAsync((void**)&derr, 16, st));
-  auto cleanup = [&]() {
-    cudaFreeAsync(dh, st);
-    cudaFreeAsync(dtmp, st);
-    cudaFreeAsync(derr, st);
-  };
-  uint64_t* dins = dtmp;
-  uint64_t* dpre = dtmp + std::max<uint64_t>(1, m);
+  const size_t hb = align256(m * sizeof(K)), pb = (m + 1) * 8;
+  DTS_TRY(g_pin_plan.ensure(hb + pb + 256));
+  char* hp = (char*)g_pin_plan.p;
+  if (m) std::memcpy(hp, hkeys, m * sizeof(K));
+  std::memcpy(hp + hb, prefix.data(), pb);
+  if (m) CUDA_TRY(cudaMemcpyAsync(dh, hp, m * sizeof(K), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(dpre, hp + hb, pb, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemsetAsync(derr, 0, 4, st));
   if (m) {
-    CUDA_TRY(cudaMemcpyAsync(dh, hkeys, m * sizeof(K), cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(dpre, prefix.data(), m * 8, cudaMemcpyHostToDevice, st));
     k_merge_layout<K><<<(unsigned)((m + 255) / 256), 256, 0, st>>>(zk, light, dh, m, dins);
-    if (check_launch("k_merge_layout")) {
-      cleanup();
-      return DTS_ECUDA;
-    }
+    DTS_TRY(check_launch("k_merge_layout"));
   }
   if (validate) {
-    CUDA_TRY(cudaMemsetAsync(derr, 0, 4, st));
     const uint64_t work = std::max<uint64_t>(total, m);
-    const unsigned grid = (unsigned)std::min<uint64_t>(4096, (work + 255) / 256 + 1);
+    const unsigned grid = (unsigned)std::min<uint64_t>(8 * device_sms(), (work + 255) / 256 + 1);
     k_merge_validate<K><<<grid, 256, 0, st>>>(zk, light, total, dh, dpre, m, dins, derr);
-    if (check_launch("k_merge_validate")) {
-      cleanup();
-      return DTS_ECUDA;
-    }
-    uint32_t err = 0;
-    CUDA_TRY(cudaMemcpyAsync(&err, derr, 4, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    if (err) {
-      cleanup();
-      if (err & 1u) return fail(DTS_EINVAL, "light run must be sorted");
-      if (err & 2u) return fail(DTS_EINVAL, "a heavy key also appears in the light run");
-      return fail(DTS_EINVAL, "heavy run contains a foreign key");
-    }
+    DTS_TRY(check_launch("k_merge_validate"));
   }
-  if (m == 0 || total == 0) {
-    cleanup();
-    CUDA_TRY(cudaStreamSynchronize(st));
-    return 0;
+  const bool permute = m > 0 && total > 0;
+  if (permute) {
+    const unsigned grid = (unsigned)std::min<uint64_t>(8 * device_sms(), (total + 255) / 256);
+    k_merge_permute<K, VB><<<grid, 256, 0, st>>>(zk, zv, light, total, dins, dpre, m, ok, ov);
+    DTS_TRY(check_launch("k_merge_permute"));
   }
-  CUDA_TRY(cudaMemcpyAsync(p.data(), dins, m * 8, cudaMemcpyDeviceToHost, st));
+  // one read-back: the error flags and the insertion points (MergeStats)
+  DTS_TRY(g_pin_back.ensure(256 + m * 8 + 256));
+  char* bp = (char*)g_pin_back.p;
+  CUDA_TRY(cudaMemcpyAsync(bp, derr, 4, cudaMemcpyDeviceToHost, st));
+  if (m) CUDA_TRY(cudaMemcpyAsync(bp + 256, dins, m * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
-  auto move = [&](K* dkp, V* dvp, const K* skp, const V* svp, uint64_t len) {
-    if (!len) return;
-    const unsigned grid = (unsigned)std::min<uint64_t>(8 * device_sms(), (len + 255) / 256);
-    k_move<K, VB><<<grid, 256, 0, st>>>(dkp, dvp, skp, svp, len);
-  };
-  auto rev = [&](uint64_t lo, uint64_t hi) {
-    if (hi - lo < 2) return;
-    const uint64_t half = (hi - lo) / 2;
-    const unsigned grid = (unsigned)std::min<uint64_t>(8 * device_sms(), (half + 255) / 256);
-    k_reverse<K, VB><<<grid, 256, 0, st>>>(zk, has_pay ? zv : nullptr, lo, hi);
-  };
-  auto shift_block = [&](uint64_t src, uint64_t len, uint64_t dest) -> uint64_t {
-    // dtmerge.py:81-105
-    if (len == 0 || dest == src) return 0;
-    rev(src, src + len);
-    if (dest < src) rev(dest, src + len);
-    else rev(src, dest + len);
-    return 2 * len;
-  };
-  V* zvp = has_pay ? zv : nullptr;
-  V* svp = has_pay ? sv : nullptr;
-  uint64_t out_copies = 0, in_moves = 0, restores = 0;
-  std::vector<uint64_t> bounds(m + 2);
-  bounds[0] = 0;
-  for (uint64_t i = 0; i < m; ++i) bounds[i + 1] = p[i];
-  bounds[m + 1] = light;
-  if (heavy_total >= light) {
-    move(sk, svp, zk, zvp, light);
-    out_copies += light;
-    for (uint64_t i = 0; i < m; ++i) {
-      const uint64_t ln = (uint64_t)hlens[i];
-      const uint64_t src = light + prefix[i];
-      const uint64_t dst = p[i] + prefix[i];
-      if (ln == 0 || dst == src) continue;
-      if (dst + ln <= src) {
-        move(zk + dst, zvp ? zvp + dst : nullptr, zk + src, zvp ? zvp + src : nullptr, ln);
-        in_moves += ln;
-      } else {
-        in_moves += shift_block(src, ln, dst);
-      }
-    }
-    for (uint64_t i = 0; i <= m; ++i) {
-      const uint64_t f0 = bounds[i], f1 = bounds[i + 1];
-      const uint64_t flen = f1 - f0;
-      const uint64_t dst = f0 + prefix[i];
-      if (flen == 0 || dst == f0) continue;
-      move(zk + dst, zvp ? zvp + dst : nullptr, sk + f0, svp ? svp + f0 : nullptr, flen);
-      restores += flen;
-    }
-  } else {
-    move(sk, svp, zk + light, zvp ? zvp + light : nullptr, heavy_total);
-    out_copies += heavy_total;
-    for (uint64_t i = m; i >= 1; --i) {
-      const uint64_t f0 = bounds[i], f1 = bounds[i + 1];
-      const uint64_t flen = f1 - f0;
-      const uint64_t dst = f0 + prefix[i];
-      if (flen == 0 || dst == f0) continue;
-      if (f0 + flen <= dst) {
-        move(zk + dst, zvp ? zvp + dst : nullptr, zk + f0, zvp ? zvp + f0 : nullptr, flen);
-        in_moves += flen;
-      } else {
-        in_moves += shift_block(f0, flen, dst);
-      }
-    }
-    for (uint64_t i = 0; i < m; ++i) {
-      const uint64_t ln = (uint64_t)hlens[i];
-      if (ln == 0) continue;
-      const uint64_t s0 = prefix[i];
-      const uint64_t dst = p[i] + prefix[i];
-      move(zk + dst, zvp ? zvp + dst : nullptr, sk + s0, svp ? svp + s0 : nullptr, ln);
-      restores += ln;
-    }
+  const uint32_t err = *(const uint32_t*)bp;
+  if (err) {  // the zone is untouched: the permutation went to the workspace
+    if (err & 1u) return fail(DTS_EINVAL, "light run must be sorted");
+    if (err & 2u) return fail(DTS_EINVAL, "a heavy key also appears in the light run");
+    return fail(DTS_EINVAL, "heavy run contains a foreign key");
   }
-  cleanup();
-  if (check_launch("dt_merge moves")) return DTS_ECUDA;
-  CUDA_TRY(cudaStreamSynchronize(st));
-  stats[0] = out_copies;
-  stats[1] = in_moves;
-  stats[2] = restores;
+  if (!permute) return 0;
+  {
+    const unsigned grid = (unsigned)std::min<uint64_t>(8 * device_sms(), (total + 255) / 256);
+    k_copy_back<K, VB><<<grid, 256, 0, st>>>(zk, zv, ok, ov, total);
+    DTS_TRY(check_launch("k_copy_back"));
+  }
+  merge_stats(light, hlens, m, (const uint64_t*)(bp + 256), prefix.data(), heavy_total, stats);
   return 0;
 }
 
@@ -1238,21 +1210,31 @@ int dts_sort(void* keys, void* vals, uint64_t n, int kb, int vb, void* ws, size_
   return sort_impl<uint64_t, 8>(keys, vals, n, ws, wsb, cfg, rep, st);
 }
 
+size_t dts_merge_workspace_bytes(uint64_t zone_len, uint64_t m, int kb, int vb) {
+  if (!valid_widths(kb, vb)) return 0;
+  return merge_ws_layout(zone_len, m, kb, vb).total;
+}
+
 int dts_merge(void* zk, void* zv, uint64_t zone_len, uint64_t light_len, const void* hkeys,
               const int64_t* hlens, uint64_t m, void* sk, void* sv, uint64_t scratch_len, int kb,
-              int vb, int validate, uint64_t stats_out[3], void* stream) {
+              int vb, int validate, void* ws, size_t wsb, uint64_t stats_out[3], void* stream) {
+  (void)sk;  // scratch keys: validated by size only (the permutation uses the workspace)
   if (!valid_widths(kb, vb)) return fail(DTS_EINVAL, "key_bytes must be 4|8 and val_bytes 0|4|8");
   if (!stats_out) return fail(DTS_EINVAL, "stats_out must not be NULL");
   if (m && (!hkeys || !hlens)) return fail(DTS_EINVAL, "heavy_keys and heavy_lens must have equal length");
   cudaStream_t st = (cudaStream_t)stream;
+#define DTS_MERGE_CALL(K, VB) \
+  merge_impl<K, VB>(zk, zv, zone_len, light_len, hkeys, hlens, m, scratch_len, sv != nullptr, validate, ws, wsb, \
+                    stats_out, st)
   if (kb == 4) {
-    if (vb == 0) return merge_impl<uint32_t, 0>(zk, zv, zone_len, light_len, hkeys, hlens, m, sk, sv, scratch_len, validate, stats_out, st);
-    if (vb == 4) return merge_impl<uint32_t, 4>(zk, zv, zone_len, light_len, hkeys, hlens, m, sk, sv, scratch_len, validate, stats_out, st);
-    return merge_impl<uint32_t, 8>(zk, zv, zone_len, light_len, hkeys, hlens, m, sk, sv, scratch_len, validate, stats_out, st);
+    if (vb == 0) return DTS_MERGE_CALL(uint32_t, 0);
+    if (vb == 4) return DTS_MERGE_CALL(uint32_t, 4);
+    return DTS_MERGE_CALL(uint32_t, 8);
   }
-  if (vb == 0) return merge_impl<uint64_t, 0>(zk, zv, zone_len, light_len, hkeys, hlens, m, sk, sv, scratch_len, validate, stats_out, st);
-  if (vb == 4) return merge_impl<uint64_t, 4>(zk, zv, zone_len, light_len, hkeys, hlens, m, sk, sv, scratch_len, validate, stats_out, st);
-  return merge_impl<uint64_t, 8>(zk, zv, zone_len, light_len, hkeys, hlens, m, sk, sv, scratch_len, validate, stats_out, st);
+  if (vb == 0) return DTS_MERGE_CALL(uint64_t, 0);
+  if (vb == 4) return DTS_MERGE_CALL(uint64_t, 4);
+  return DTS_MERGE_CALL(uint64_t, 8);
+#undef DTS_MERGE_CALL
 }
 
 int dts_partition(const void* keys, const void* vals, uint64_t n, uint64_t gbase,
@@ -1260,7 +1242,8 @@ int dts_partition(const void* keys, const void* vals, uint64_t n, uint64_t gbase
                   void* ovals, uint64_t* counts, int kb, int vb, void* ws, size_t wsb,
                   void* stream) {
   if (!valid_widths(kb, vb)) return fail(DTS_EINVAL, "key_bytes must be 4|8 and val_bytes 0|4|8");
-  if (nsplit < 0 || nsplit > 4095) return fail(DTS_EINVAL, "nsplit must be in [0, 4095]");
+  if (nsplit < 0 || nsplit >= ScatterTile<uint32_t, 4>::HKC)
+    return fail(DTS_EINVAL, "nsplit must be in [0, 1023]");  // SMEM splitter / bucket tables (ScatterTile HKC, NBC)
   if (!counts) return fail(DTS_EINVAL, "send_counts must not be NULL");
   if (nsplit && (!split_keys || !split_idx)) return fail(DTS_EINVAL, "splitters must not be NULL");
   cudaStream_t st = (cudaStream_t)stream;

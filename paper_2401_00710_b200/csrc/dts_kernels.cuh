@@ -591,8 +591,8 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(const SegPlan* __restrict__
 }
 
 // ---------------------------------------------------------------------------
-// Dovetail-merge pieces (dtmerge.py).  The host runs the reference's piece
-// loop and launches these grid-parallel moves.
+// Dovetail merge (dtmerge.py): insertion points, validation, and the
+// out-of-place permutation of the whole zone.
 // ---------------------------------------------------------------------------
 template <typename K>
 __global__ void k_merge_layout(const K* __restrict__ light, uint64_t light_len,
@@ -637,33 +637,47 @@ __global__ void k_merge_validate(const K* __restrict__ zone, uint64_t light_len,
   }
 }
 
+// Layout-driven out-of-place merge permutation (dtmerge.py:58-78 layout, the
+// result of :132-238): light record j lands at j + (heavy records whose key
+// is below it) = j + hprefix[#{i : ins[i] <= j}]; heavy record r of run i at
+// ins[i] + hprefix[i] + r.  One pass over the zone into the workspace copy.
 template <typename K, int VB>
-__global__ void k_move(K* __restrict__ dk, typename ValOf<VB>::T* __restrict__ dv,
-                       const K* __restrict__ sk, const typename ValOf<VB>::T* __restrict__ sv,
-                       uint64_t len) {
+__global__ void k_merge_permute(const K* __restrict__ zk, const typename ValOf<VB>::T* __restrict__ zv,
+                                uint64_t light_len, uint64_t total, const uint64_t* __restrict__ ins,
+                                const uint64_t* __restrict__ hprefix, uint64_t m, K* __restrict__ ok,
+                                typename ValOf<VB>::T* __restrict__ ov) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += stride) {
-    dk[i] = sk[i];
-    if (VB) dv[i] = sv[i];
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < total; s += stride) {
+    uint64_t d;
+    if (s < light_len) {
+      uint64_t lo = 0, hi = m;  // #{i : ins[i] <= s}
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (ins[mid] <= s) lo = mid + 1; else hi = mid;
+      }
+      d = s + hprefix[lo];
+    } else {
+      const uint64_t h = s - light_len;
+      uint64_t lo = 0, hi = m;  // run i: hprefix[i] <= h < hprefix[i + 1]
+      while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (hprefix[mid] <= h) lo = mid; else hi = mid;
+      }
+      d = ins[lo] + h;
+    }
+    ok[d] = zk[s];
+    if (VB && zv) ov[d] = zv[s];
   }
 }
 
 template <typename K, int VB>
-__global__ void k_reverse(K* __restrict__ k, typename ValOf<VB>::T* __restrict__ v, uint64_t lo,
-                          uint64_t hi) {
-  // reverse_range (_kernels.py:28-38): pairs (lo+i, hi-1-i) swap independently.
-  const uint64_t half = (hi - lo) / 2;
+__global__ void k_copy_back(K* __restrict__ dk, typename ValOf<VB>::T* __restrict__ dv,
+                            const K* __restrict__ sk, const typename ValOf<VB>::T* __restrict__ sv,
+                            uint64_t len) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < half; i += stride) {
-    const uint64_t a = lo + i, b = hi - 1 - i;
-    const K t = k[a];
-    k[a] = k[b];
-    k[b] = t;
-    if (VB) {
-      const typename ValOf<VB>::T u = v[a];
-      v[a] = v[b];
-      v[b] = u;
-    }
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += stride) {
+    dk[i] = sk[i];
+    if (VB && dv) dv[i] = sv[i];
   }
 }
 

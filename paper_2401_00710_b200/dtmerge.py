@@ -1,10 +1,12 @@
 """Dovetail merge on the B200 (drop-in for dtmerge.py:132-238).
 
 Same signature, validation order and messages as the reference; the zone
-is merged in place.  The heavy-key insertion points are computed by a GPU
-binary-search kernel and every piece move (direct copy or two-flip shift,
-dtmerge.py:81-105) is a grid-parallel kernel, so ``MergeStats`` equals the
-reference's exactly.  The sort path itself does not call this: the scatter
+is merged in place.  On the GPU (include/dts.h dts_merge) the heavy-key
+insertion points come from a binary-search kernel, and the zone is permuted
+out of place in one pass into a workspace and copied back (3-4 launches,
+one read-back); ``MergeStats`` are the reference's piece-loop counts
+(direct copy or two-flip shift, dtmerge.py:81-105), computed on the host
+from the insertion points, so they equal the reference's exactly.  The sort path itself does not call this: the scatter
 places heavy runs at their merged positions directly.
 """
 from __future__ import annotations
@@ -32,6 +34,18 @@ class MergeStats:
 
 def _len(x) -> int:
     return int(x.shape[0])
+
+
+def _width(x) -> int:
+    return int(x.element_size() if _is_torch(x) else np.asarray(x).itemsize)
+
+
+def _addr(x) -> int:
+    """Address of a scratch array (never dereferenced by dts_merge; non-null
+    tells it scratch payloads were supplied)."""
+    if _is_torch(x):
+        return int(x.data_ptr()) or 1
+    return int(np.asarray(x).ctypes.data) or 1
 
 
 def dt_merge(
@@ -73,30 +87,31 @@ def dt_merge(
     with torch.cuda.device(device):
         zk = Column(zone_keys, device, None)
         zv = Column(zone_payloads, device, None) if has_pay else None
-        sk = Column(scratch_keys, device, None)
-        sv = Column(scratch_payloads, device, None) if has_pay else None
         kb = zk.width
         vb = 0 if zv is None else zv.width
-        if sk.width != kb or (sv is not None and sv.width != vb):
+        # scratch is validated (the reference's contract) but not written:
+        # the GPU permutes the zone through a workspace
+        if _width(scratch_keys) != kb or (has_pay and _width(scratch_payloads) != vb):
             raise ValueError("scratch dtype must match the zone's")
         stats = (ctypes.c_uint64 * 3)()
         stream = torch.cuda.current_stream(device).cuda_stream
-        rc = _lib.lib().dts_merge(
+        L = _lib.lib()
+        wsb = int(L.dts_merge_workspace_bytes(total, m, kb, vb))
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=device)
+        rc = L.dts_merge(
             ctypes.c_void_p(zk.ptr()),
             ctypes.c_void_p(0 if zv is None else zv.ptr()),
             total, light_len,
             ctypes.c_void_p(hk.ctypes.data if m else 0),
             hl.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
             m,
-            ctypes.c_void_p(sk.ptr()),
-            ctypes.c_void_p(0 if sv is None else sv.ptr()),
-            _len(scratch_keys), kb, vb, int(bool(validate)), stats, ctypes.c_void_p(stream),
+            ctypes.c_void_p(_addr(scratch_keys)),
+            ctypes.c_void_p(_addr(scratch_payloads) if has_pay else 0),
+            _len(scratch_keys), kb, vb, int(bool(validate)), ctypes.c_void_p(ws.data_ptr()), wsb, stats,
+            ctypes.c_void_p(stream),
         )
         _lib.check(rc)
         zk.writeback()
         if zv is not None:
             zv.writeback()
-        sk.writeback()
-        if sv is not None:
-            sv.writeback()
     return MergeStats(int(stats[0]), int(stats[1]), int(stats[2]))

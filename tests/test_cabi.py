@@ -36,7 +36,7 @@ def test_library_exports_every_header_symbol():
 
 def test_abi_version_arch_and_workspace():
     L = _lib.lib()
-    assert L.dts_abi_version() == 1
+    assert L.dts_abi_version() == 2  # 2: dts_merge takes a workspace
     assert L.dts_build_arch() == 100
     n = 10**6
     ws = L.dts_workspace_bytes(n, 4, 4)
@@ -77,3 +77,20 @@ def test_oversized_call_is_rejected_before_touching_the_device():
     dummy = ctypes.c_void_p(16)
     rc = L.dts_sort(dummy, None, 1 << 32, 4, 0, None, 0, ctypes.byref(cfg), None, None)
     assert rc == -1 and b"2^32" in L.dts_last_error()
+
+
+def test_partition_rejects_more_splitters_than_its_tables_hold():
+    """G <= 1024: the splitter / bucket tables of the partition scatter live in
+    shared memory (ScatterTile HKC = NBC = 1024)."""
+    import ctypes
+
+    import numpy as np
+
+    L = _lib.lib()
+    sk = np.zeros(1024, np.uint32)
+    si = np.zeros(1024, np.uint64)
+    counts = np.zeros(1025, np.uint64)
+    P64 = ctypes.POINTER(ctypes.c_uint64)
+    rc = L.dts_partition(None, None, 0, 0, ctypes.c_void_p(sk.ctypes.data), si.ctypes.data_as(P64), 1024,
+                         None, None, counts.ctypes.data_as(P64), 4, 4, None, 0, None)
+    assert rc == -1 and b"1023" in L.dts_last_error()

@@ -13,13 +13,12 @@ G = pathlib.Path(__file__).resolve().parent / "golden"
 
 
 def test_gpu_dt_merge_exhaustive_grid_matches_reference():
+    """All 4480 cases of test_dtmerge.py:62-82's grid."""
     from paper_2401_00710_b200 import dt_merge
 
     g = np.load(G / "merge_golden.npz")
     offs = g["offsets"]
     for i, (light, heavy) in enumerate(cases.merge_grid()):
-        if i % 7:  # every 7th case of the 4480 (keeps the GPU test short)
-            continue
         keys, pays = cases.build_zone(light, heavy)
         hk = np.array([k for k, _ in heavy], dtype=np.uint32)
         hl = np.array([ln for _, ln in heavy], dtype=np.int64)
@@ -43,8 +42,6 @@ def test_gpu_dt_merge_random_zones_match_reference():
         light = np.sort(rng.integers(0, universe, size=light_len) * 2)
         hk = np.sort(rng.choice(universe, size=min(m, universe), replace=False) * 2 + 1)
         heavy = [(int(k), int(rng.integers(0, 40))) for k in hk]
-        if trial % 4:
-            continue
         dt = np.uint64 if r["wide"] else np.uint32
         keys, pays = cases.build_zone(light.tolist(), heavy, dt)
         hka = np.array([k for k, _ in heavy], dtype=dt)
@@ -106,8 +103,10 @@ def test_gpu_dt_merge_large_zone():
 
 
 @pytest.mark.parametrize("kb,vb", [(4, 4), (8, 8), (4, 0)])
-@pytest.mark.parametrize("G_", [1, 2, 3, 8])
+@pytest.mark.parametrize("G_", [1, 2, 3, 8, 17, 64, 1024])
 def test_gpu_partition_matches_host_model(kb, vb, G_):
+    """G <= 16: the prefix-table splitter router; G >= 17: the binary-search
+    router; 1024 = the largest G dts_partition accepts."""
     import torch
 
     from paper_2401_00710_b200.distributed import CudaOps, choose_splitters
@@ -115,14 +114,20 @@ def test_gpu_partition_matches_host_model(kb, vb, G_):
     rng = np.random.default_rng(G_ * 10 + kb)
     n = 500_000
     kdt = np.uint32 if kb == 4 else np.uint64
-    keys = rng.integers(0, 1000, size=n).astype(kdt)
+    hi_key = 1000 if G_ <= 8 else (1 << 30)
+    keys = rng.integers(0, hi_key, size=n).astype(kdt)
+    if G_ > 8:
+        keys[rng.random(n) < 0.2] = 777  # splitters inside one key's run
     gbase = 12345
     gidx = np.arange(n, dtype=np.uint64) + np.uint64(gbase)
-    samp = rng.integers(0, n, size=4096)
+    samp = rng.integers(0, n, size=max(4096, 8 * G_))
     spk, spi = choose_splitters(keys[samp], gidx[samp], G_)
-    dest = np.zeros(n, np.int64)
-    for sk, si in zip(spk, spi):
-        dest += (keys > sk) | ((keys == sk) & (gidx > si))
+    # dest = #splitters strictly below (key, global index), lexicographic
+    lo = np.searchsorted(spk, keys, side="left").astype(np.int64)
+    hi = np.searchsorted(spk, keys, side="right").astype(np.int64)
+    dest = lo.copy()
+    for i in np.nonzero(hi > lo)[0]:
+        dest[i] += int(np.count_nonzero(spi[lo[i]:hi[i]] < gidx[i]))
     order = np.argsort(dest, kind="stable")
     vals = None if vb == 0 else np.arange(n, dtype=np.uint32 if vb == 4 else np.uint64)
     tk = torch.from_numpy(keys.view(np.int32 if kb == 4 else np.int64).copy()).cuda()

@@ -163,8 +163,14 @@ def test_gpu_heavy_keys_and_overflow_counters():
     rec = RecordArray(keys.copy(), pays.copy())
     rep = dt_sort(rec, SortConfig(instrument=True))
     assert np.array_equal(rec.keys, want_k) and np.array_equal(rec.payloads, want_v)
-    # the planted key got its own bucket (3 outliers may overwrite planted slots)
+    # the planted key got its own bucket (3 outliers may overwrite planted
+    # slots) — in the reference's counters (host replay) AND in the GPU
+    # pipeline's own structure (rep.gpu: k_sample_plan's heavy set)
     assert rep.heavy_records_removed[0] >= n // 3 - 3
+    assert rep.gpu.heavy_records_removed[0] >= n // 3 - 3
+    assert rep.gpu.kernel_records["sample"] >= 1
+    # the outliers sit above the sampled maximum: the GPU root skip fired
+    assert rep.gpu.skipped_bits > 0
     assert rep.records_distributed >= n
 
 
