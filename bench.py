@@ -573,7 +573,7 @@ def main():
     cfgd = dict(CONFIGS[args.config])
     if args.n:
         cfgd["n"] = args.n
-    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+    if "WORLD_SIZE" not in os.environ and (args.gpus > 1 or (args.force_dist and args.impl == "ours")):
         # `python bench.py --gpus N` outside torchrun: launch N ranks (one per
         # GPU) under torch.distributed.run on 127.0.0.1 and relay rank 0's line
         sys.exit(self_launch(args))

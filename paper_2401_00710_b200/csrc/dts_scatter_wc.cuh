@@ -441,12 +441,28 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
         }
       };
       {
-        bool bad = false;
-        for (uint32_t p = tid; p + 1 < tn; p += NT) {
-          const bool same = !((bend[p >> 5] >> (p & 31)) & 1u);
-          bad |= same & (pk[p + 1] < pk[p]);
+        // 8 staging slots per thread: one 16-byte load of their tile
+        // positions, packed u16 compares of every adjacent pair, masked by
+        // the run-end bits (a pair across two bucket runs is not checked)
+        uint32_t bad = 0u;
+        const uint4* pk4 = reinterpret_cast<const uint4*>(pk);
+        for (uint32_t q = tid; 8 * q + 1 < tn; q += NT) {
+          const uint4 X = pk4[q];
+          const uint32_t x8 = pk[8 * q + 8];  // (pk has T + 2 entries)
+          const uint32_t S0 = __byte_perm(X.x, X.y, 0x5432), S1 = __byte_perm(X.y, X.z, 0x5432);
+          const uint32_t S2 = __byte_perm(X.z, X.w, 0x5432), S3 = __byte_perm(X.w, x8, 0x5432);
+          // byte j = 0xff when pair (8q+j, 8q+j+1) descends
+          const uint32_t lo = __byte_perm(__vcmpltu2(S0, X.x), __vcmpltu2(S1, X.y), 0x6420);
+          const uint32_t hi = __byte_perm(__vcmpltu2(S2, X.z), __vcmpltu2(S3, X.w), 0x6420);
+          // pairs inside one run and inside the tile: bit j of `in`
+          const uint32_t p0 = 8 * q;
+          const uint32_t lim = tn - 1 - p0;  // pairs j < lim are inside the tile
+          uint32_t in = ~(bend[p0 >> 5] >> (p0 & 31)) & (lim >= 8 ? 0xffu : ((1u << lim) - 1u));
+          const uint32_t inlo = ((in & 15u) * 0x00204081u) & 0x01010101u;
+          const uint32_t inhi = (((in >> 4) & 15u) * 0x00204081u) & 0x01010101u;
+          bad |= (lo & inlo) | (hi & inhi);
         }
-        if (__any_sync(FULL, bad) && lane == 0) s_fix = 1u;
+        if (__any_sync(FULL, bad != 0u) && lane == 0) s_fix = 1u;
       }
       write_chunks();
       __syncthreads();
