@@ -137,6 +137,10 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
   __shared__ Blk s_B;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t* mywh = wh + warp * HW;
+  // key and value of the same width: staging slots and carry slots are
+  // (key, value) pairs (AoS), one SMEM access per record
+  constexpr bool AOS = VB == (int)sizeof(K);
+  using PairT = typename StPair<K>::T;
 
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -231,7 +235,6 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       V* xv = bufv(cur);
       // staging slot accessors (AoS pairs when key and value widths match;
       // the pair array spans this tile's key+value buffer)
-      constexpr bool AOS = VB == (int)sizeof(K);
       auto st_put = [&](uint32_t p, K k, V v) {
         if constexpr (AOS) {
           reinterpret_cast<typename StPair<K>::T*>(xk)[p] = StPair<K>::make(k, (K)v);
@@ -422,13 +425,23 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       // run (carry slots [0, cc) first, then the staging run) ----
       auto write_chunks = [&]() {
         const uint32_t nslot = nch * C;
+        const uint32_t stoff = (uint32_t)(SL::buf + (size_t)cur * (SL::kb + SL::vb));  // staging pairs
         for (uint32_t q = tid; q < nslot; q += NT) {
           const uint2 D = cdesc[q / C];
           const uint32_t r = q % C;
           if (r < ((D.y >> 18) & 15u)) continue;  // hole: the previous stripe's records
           K kk;
           V vv = V(0);
-          if (r < ((D.y >> 14) & 15u)) {
+          if constexpr (AOS) {
+            // carry slot or staging slot: both are (key, value) pairs — one
+            // select of the SMEM offset, one load, no divergent branch
+            const uint32_t off = r < ((D.y >> 14) & 15u)
+                                     ? (uint32_t)SL::ck + ((D.y >> 22) * CP + r) * (uint32_t)sizeof(PairT)
+                                     : stoff + ((D.y & 0x3FFFu) - 16u + r) * (uint32_t)sizeof(PairT);
+            const PairT pr = *reinterpret_cast<const PairT*>(smem_raw + off);
+            kk = pr.x;
+            vv = (V)pr.y;
+          } else if (r < ((D.y >> 14) & 15u)) {
             const uint32_t b = D.y >> 22;
             kk = ck[b * CP + r];
             if (VB) vv = cv[b * CP + r];
@@ -517,22 +530,38 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
             const uint32_t b = b0 + u * NW * BPW + sub;
             dw[u] = b < nb ? bnf[b] : 0u;
           }
-          K tk[U];
-          V tv[U];
+          if constexpr (AOS) {
+            const PairT* sp = reinterpret_cast<const PairT*>(xk);
+            PairT* cpr = reinterpret_cast<PairT*>(smem_raw + SL::ck);
+            PairT tp[U];
 #pragma unroll
-          for (uint32_t u = 0; u < U; ++u) {
-            if (i < (dw[u] >> 24)) {
-              const uint32_t src = (dw[u] & 0xffffu) + i;
-              st_get(src, tk[u], tv[u]);
+            for (uint32_t u = 0; u < U; ++u)
+              if (i < (dw[u] >> 24)) tp[u] = sp[(dw[u] & 0xffffu) + i];
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u) {
+              if (i < (dw[u] >> 24)) {
+                const uint32_t b = b0 + u * NW * BPW + sub;
+                cpr[b * CP + ((dw[u] >> 16) & 0xffu) + i] = tp[u];
+              }
             }
-          }
+          } else {
+            K tk[U];
+            V tv[U];
 #pragma unroll
-          for (uint32_t u = 0; u < U; ++u) {
-            if (i < (dw[u] >> 24)) {
-              const uint32_t b = b0 + u * NW * BPW + sub;
-              const uint32_t dst = b * CP + ((dw[u] >> 16) & 0xffu) + i;
-              ck[dst] = tk[u];
-              if (VB) cv[dst] = tv[u];
+            for (uint32_t u = 0; u < U; ++u) {
+              if (i < (dw[u] >> 24)) {
+                const uint32_t src = (dw[u] & 0xffffu) + i;
+                st_get(src, tk[u], tv[u]);
+              }
+            }
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u) {
+              if (i < (dw[u] >> 24)) {
+                const uint32_t b = b0 + u * NW * BPW + sub;
+                const uint32_t dst = b * CP + ((dw[u] >> 16) & 0xffu) + i;
+                ck[dst] = tk[u];
+                if (VB) cv[dst] = tv[u];
+              }
             }
           }
         }
@@ -551,8 +580,14 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
         if (b < nb) {
           const uint2 I = cst[b];
           if (r >= (I.x >> 16) && r < (I.x & 0xffffu)) {
-            st_global(ko_seg + I.y + r, ck[b * CP + r]);
-            if (VB) st_global(vo_seg + I.y + r, cv[b * CP + r]);
+            if constexpr (AOS) {
+              const PairT pr = reinterpret_cast<const PairT*>(smem_raw + SL::ck)[b * CP + r];
+              st_global(ko_seg + I.y + r, (K)pr.x);
+              st_global(vo_seg + I.y + r, (V)pr.y);
+            } else {
+              st_global(ko_seg + I.y + r, ck[b * CP + r]);
+              if (VB) st_global(vo_seg + I.y + r, cv[b * CP + r]);
+            }
           }
         }
       }
