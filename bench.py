@@ -276,16 +276,24 @@ def run_ours(args, cfgd, rank, world, local_rank):
         restore()
         one_sort()
     torch.cuda.synchronize()
-    # correctness certificate on the last warm-up output (values = index)
-    if not multi and v is not None and kb == 4:
-        ok = True
-        for c0 in range(0, n - 1, 1 << 28):  # chunked (no n-sized int64 temporaries)
-            c1 = min(n, c0 + (1 << 28) + 1)
-            kk = k[c0:c1].to(torch.int64) & 0xFFFFFFFF
-            ok &= bool((kk[1:] >= kk[:-1]).all())
-        if not ok:
-            raise SystemExit("sorted-order check failed")
+    # correctness certificate on the last warm-up output (paper_2401_00710_b200/
+    # certify.py): values = index -> the O(n) stable-sort certificate; C5
+    # (values = src) and keys-only C1 -> sorted keys + the permutation-invariant
+    # pair checksum of the input
+    cert = None
+    if not multi:
+        from paper_2401_00710_b200 import certify
 
+        if v is not None and cfgd["dist"] != "rmat":
+            err = certify.stable_sort_certificate(src_k, k, v)
+            cert = "stable-sort certificate (sorted, permutation, stable, key[i] == in[val[i]])"
+        else:
+            err = None if certify.keys_sorted(k) else "keys not sorted"
+            if err is None and certify.pair_checksum(k, v) != certify.pair_checksum(src_k, src_v):
+                err = "output records are not a permutation of the input records"
+            cert = "sorted keys + permutation-invariant (key, value) checksum"
+        if err is not None:
+            raise SystemExit(f"certificate failed on the last warm-up output: {err}")
     clocks = Clocks(local_rank)
     if multi:
         dist.barrier()
@@ -478,7 +486,8 @@ def run_ours(args, cfgd, rank, world, local_rank):
             "config": {"workload": args.config, "desc": cfgd["desc"], "n_per_gpu": n,
                        "key_bytes": kb, "val_bytes": vb, "parallelism": f"keyrange{world}" if multi else "single",
                        "l2": "inputs (n*(k+v) bytes) exceed the 126 MB L2; no flush needed",
-                       "timed": "CUDA events around each sort; per-step input restore outside"},
+                       "timed": "CUDA events around each sort; per-step input restore outside",
+                       "checked": cert},
             "roofline": roof, "pipeline_roofline": pipe, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk,
         }
