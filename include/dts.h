@@ -150,6 +150,20 @@ int dts_csr_offsets(const void* keys, uint64_t n, int key_bytes, uint64_t nverts
 /* Message for the last nonzero status on this thread. */
 const char* dts_last_error(void);
 
+/* Morton (z-order) keys of n points — the paper's Morton-sort application
+ * (PAPER.md:1149-1165): keys[i] interleaves the low `bits` bits of the
+ * point's coordinates (x, y[, z]: device arrays of uint32; dims 2 or 3; bits
+ * <= 32 for 2-D, <= 21 for 3-D), coordinate 0 in the lowest bit of each
+ * group: bit dims*i + c of the key = bit i of coordinate c.  vals (may be
+ * NULL) receives first_index + i, the payload that makes dts_sort(keys,
+ * vals) a Morton sort returning the point permutation.  workspace: >= 16
+ * device bytes.  DTS_EINVAL (and keys written) when a coordinate has a bit
+ * at or above `bits`.  Blocks once (the range check). */
+int dts_morton_keys(const uint32_t* x, const uint32_t* y, const uint32_t* z,
+                    uint64_t n, int dims, int bits, uint64_t* keys,
+                    uint64_t* vals, uint64_t first_index, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
 /* DTS_ABI_VERSION and the SM architecture the library was built for (100). */
 int dts_abi_version(void);
 int dts_build_arch(void);

@@ -120,6 +120,14 @@ SIGNATURES = (
             ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
         ],
     ),
+    (
+        "dts_morton_keys",
+        ctypes.c_int,
+        [
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+        ],
+    ),
     ("dts_last_error", ctypes.c_char_p, []),
     ("dts_abi_version", ctypes.c_int, []),
     ("dts_build_arch", ctypes.c_int, []),

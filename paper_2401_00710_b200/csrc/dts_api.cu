@@ -21,6 +21,7 @@
 #include "dts_scatter.cuh"
 #include "dts_scatter_wc.cuh"
 #include "dts_graph.cuh"
+#include "dts_morton.cuh"
 
 using namespace dts;
 
@@ -1334,6 +1335,30 @@ int dts_csr_offsets(const void* keys, uint64_t n, int kb, uint64_t nverts, uint6
     k_csr_fill_gaps<<<h[0], 256, 0, st>>>(gaps, flags, row_ptr);
     DTS_TRY(check_launch("k_csr_fill_gaps"));
   }
+  return 0;
+}
+
+int dts_morton_keys(const uint32_t* x, const uint32_t* y, const uint32_t* z, uint64_t n, int dims, int bits,
+                    uint64_t* keys, uint64_t* vals, uint64_t first_index, void* ws, size_t wsb, void* stream) {
+  if (dims != 2 && dims != 3) return fail(DTS_EINVAL, "dims must be 2 or 3");
+  if (bits < 1 || bits > (dims == 2 ? 32 : 21))
+    return fail(DTS_EINVAL, "bits per coordinate must be in [1, 32] (2-D) or [1, 21] (3-D)");
+  if (!ws || wsb < 16) return fail(DTS_ENOMEM, "workspace too small for dts_morton_keys (16 bytes)");
+  if (n == 0) return 0;
+  if (!x || !y || (dims == 3 && !z) || !keys) return fail(DTS_EINVAL, "coordinate and key arrays must not be NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* flags = (uint32_t*)ws;
+  CUDA_TRY(cudaMemsetAsync(flags, 0, 4, st));
+  const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, (uint64_t)device_sms() * 16);
+  if (dims == 2)
+    k_morton<2><<<(unsigned)blocks, 256, 0, st>>>(x, y, nullptr, n, (uint32_t)bits, keys, vals, first_index, flags);
+  else
+    k_morton<3><<<(unsigned)blocks, 256, 0, st>>>(x, y, z, n, (uint32_t)bits, keys, vals, first_index, flags);
+  DTS_TRY(check_launch("k_morton"));
+  uint32_t h = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h, flags, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (h) return fail(DTS_EINVAL, "a coordinate does not fit in `bits` bits");
   return 0;
 }
 

@@ -1,7 +1,9 @@
-"""Dataset layer and CLI: generators and the ISRT
-writer byte-identical to the reference (golden SHA-256 from
-tests/golden/make_datasets_golden.py), reader validation messages, and the
-host-only CLI commands.  GPU subcommands are in test_gpu_cli.py."""
+"""Dataset layer: the harness port of the
+reference's generators (harness/refgen.py) and the ISRT writer
+(paper_2401_00710_b200/isrt.py) byte-identical to the reference (golden
+SHA-256 from tests/golden/make_datasets_golden.py), reader validation
+messages, and the CLI's `gen`.  The device subcommands are in
+test_gpu_cli.py."""
 import hashlib
 import json
 import pathlib
@@ -10,7 +12,8 @@ import numpy as np
 import pytest
 
 from paper_2401_00710_b200.core import RecordArray
-from paper_2401_00710_b200.datasets import DistSpec, generate, generate_edges, read_dataset, write_dataset
+from harness.refgen import DistSpec, generate, generate_edges
+from paper_2401_00710_b200.isrt import read_dataset, read_header, write_dataset
 
 G = json.loads((pathlib.Path(__file__).resolve().parent / "golden" / "datasets_golden.json").read_text())
 
@@ -70,17 +73,35 @@ def test_distspec_validation():
         DistSpec("bexp", 0.5, 10)
 
 
-def test_cli_gen_and_verify_host_only(tmp_path, capsys):
-    from paper_2401_00710_b200.cli import main, reference_sort
+def test_cli_gen_writes_the_reference_bytes(tmp_path, capsys):
+    from paper_2401_00710_b200.cli import main
 
     f = tmp_path / "d.isrt"
     assert main(["gen", "--dist", "zipf", "--param", "1.2", "--n", "20000", "--out", str(f)]) == 0
     assert "wrote 20000 32-bit records (zipf 1.2)" in capsys.readouterr().out
-    recs, _ = read_dataset(f)
-    srt = reference_sort(recs)
-    write_dataset(tmp_path / "s.isrt", srt)
-    assert main(["verify", "--in", str(tmp_path / "s.isrt")]) == 0
-    assert "verified: stable sort output of 20000 records" in capsys.readouterr().out
-    assert main(["verify", "--in", str(f)]) == 1  # unsorted input is rejected
-    assert main(["sort", "--algo", "baseline", "--in", str(f), "--verify", "--out", str(tmp_path / "b.isrt")]) == 0
-    assert "verified=ok" in capsys.readouterr().out
+    recs, pw = read_dataset(f)
+    want = generate(DistSpec("zipf", 1.2, 20000))
+    assert pw == 8 and np.array_equal(recs.keys, want.keys) and np.array_equal(recs.payloads, want.payloads)
+    h = read_header(f)
+    assert (h.key_bits, h.payload_width, h.count) == (32, 8, 20000)
+
+
+def test_isrt_chunked_write_and_empty_file(tmp_path):
+    import paper_2401_00710_b200.isrt as isrt
+
+    isrt._CHUNK, old = 1000, isrt._CHUNK  # several chunks
+    try:
+        r = generate(DistSpec("exp", 2.0, 4321, 64, 3))
+        for pw in (0, 4, 8):
+            p = tmp_path / f"x{pw}.isrt"
+            write_dataset(p, r if pw else RecordArray(r.keys), payload_width=pw)
+            back, bpw = read_dataset(p)
+            assert bpw == pw and np.array_equal(back.keys, r.keys)
+            if pw:
+                assert np.array_equal(back.payloads, r.payloads)
+    finally:
+        isrt._CHUNK = old
+    e = tmp_path / "e.isrt"
+    write_dataset(e, RecordArray(np.empty(0, np.uint32)))
+    back, pw = read_dataset(e)
+    assert len(back) == 0 and pw == 0

@@ -1,4 +1,5 @@
 """GPU subcommands of the CLI (the reference's harness, bench.py:238-391)."""
+import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -35,3 +36,35 @@ def test_cli_transpose_and_theory(capsys):
     assert "transposed 200000 edges over 5000 vertices" in out and "stability check: ok" in out
     assert main(["theory-check", "--sizes", "100000", "1000000"]) == 0
     assert "accounting bounds hold" in capsys.readouterr().out
+
+
+def test_cli_verify_and_baseline_sort(tmp_path, capsys):
+    from harness.refgen import DistSpec, generate
+    from paper_2401_00710_b200.cli import main, reference_sort
+    from paper_2401_00710_b200.isrt import read_dataset, write_dataset
+
+    f = tmp_path / "d.isrt"
+    assert main(["gen", "--dist", "zipf", "--param", "1.2", "--n", "20000", "--out", str(f)]) == 0
+    capsys.readouterr()
+    recs, _ = read_dataset(f)
+    write_dataset(tmp_path / "s.isrt", reference_sort(recs))
+    for algo in ("baseline", "dtsort", "plain"):
+        assert main(["verify", "--in", str(tmp_path / "s.isrt"), "--algo", algo]) == 0
+        assert "verified: stable sort output of 20000 records" in capsys.readouterr().out
+    assert main(["verify", "--in", str(f)]) == 1  # unsorted input is rejected
+    assert main(["sort", "--algo", "baseline", "--in", str(f), "--verify", "--out", str(tmp_path / "b.isrt")]) == 0
+    assert "verified=ok" in capsys.readouterr().out
+    # a file whose equal keys are out of input order is not a stable sort
+    bad = reference_sort(recs)
+    k = bad.keys
+    i = int(np.nonzero(k[1:] == k[:-1])[0][0])
+    p = bad.payloads.copy()
+    p[i], p[i + 1] = p[i + 1], p[i]
+    write_dataset(tmp_path / "u.isrt", type(bad)(k, p))
+    assert main(["verify", "--in", str(tmp_path / "u.isrt")]) == 1
+    # 4-byte payloads round-trip through the device path
+    write_dataset(tmp_path / "p4.isrt", recs, payload_width=4)
+    assert main(["sort", "--in", str(tmp_path / "p4.isrt"), "--verify", "--out", str(tmp_path / "p4s.isrt")]) == 0
+    back, pw = read_dataset(tmp_path / "p4s.isrt")
+    want = reference_sort(recs)
+    assert pw == 4 and np.array_equal(back.keys, want.keys) and np.array_equal(back.payloads, want.payloads)

@@ -162,7 +162,7 @@ def test_theory_mode_threshold():
 def test_criterion_5_work_bound_shape(bits, level_cap):
     """test_acceptance.py:161-170"""
     from paper_2401_00710_b200 import SortConfig, dt_sort
-    from paper_2401_00710_b200.datasets import DistSpec, generate
+    from harness.refgen import DistSpec, generate
 
     for n in (10**5, 10**6, 10**7):
         data = generate(DistSpec("uniform", float(2**bits), n, bits, 1))
@@ -177,7 +177,7 @@ def test_criterion_6_duplicate_advantage(mu):
     """test_acceptance.py:173-192 (20 seeds instead of 100: the bound is
     per seed, and the reference asks for >= 99/100)"""
     from paper_2401_00710_b200 import SortConfig, dt_sort, plain_msd_sort
-    from paper_2401_00710_b200.datasets import DistSpec, generate
+    from harness.refgen import DistSpec, generate
 
     n, trials = 10**6, 20
     mass_ok = moves_ok = 0
