@@ -385,13 +385,25 @@ def run_ours(args, cfgd, rank, world, local_rank):
                 "algorithmic_bytes_per_launch": int(per_launch_bytes),
                 "ms_per_launch": round(per_launch_ms, 4),
                 "step_share": shares}
-        # D of the reference's own distribution structure (SURVEY.md §8d
-        # table, wrapper-measured on these configs), scaled to --n
-        D_ref = 3 * n if args.config == "c2" else (
-            int(cfgd["D_ref"] * n / CONFIGS[args.config]["n"]) if "D_ref" in cfgd else None)
+        # D of the reference's own distribution structure on THIS input:
+        # profiles/D_exact.json (tools/d_exact.py: the oracle's
+        # records_distributed on bench.py's exact rank-0 input); else the
+        # SURVEY.md §8d table value scaled to --n
+        D_ref, D_src = None, None
+        try:
+            with open(os.path.join(ROOT, "profiles", "D_exact.json")) as f:
+                dx = json.load(f).get(args.config)
+            if dx and int(dx["n"]) == n:
+                D_ref, D_src = int(dx["D"]), "exact (oracle on this input, profiles/D_exact.json)"
+        except Exception:
+            pass
+        if D_ref is None:
+            D_ref = 3 * n if args.config == "c2" else (
+                int(cfgd["D_ref"] * n / CONFIGS[args.config]["n"]) if "D_ref" in cfgd else None)
+            D_src = "SURVEY.md §8d table" if D_ref is not None else None
         D_ours = reps[0].records_distributed
         beta = kb + 2 * (kb + vb)
-        pipe = {"beta_bytes": beta, "D_ours": D_ours, "D_reference": D_ref,
+        pipe = {"beta_bytes": beta, "D_ours": D_ours, "D_reference": D_ref, "D_reference_source": D_src,
                 "B_alg_GB": round(beta * (D_ref or D_ours) / 1e9, 3),
                 "achieved_GBps": round(beta * (D_ref or D_ours) / (ms / 1e3) / 1e9, 1),
                 "frac_of_peak": round(beta * (D_ref or D_ours) / (ms / 1e3) / 1e9 / peak, 4)}

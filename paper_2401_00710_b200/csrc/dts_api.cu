@@ -315,6 +315,7 @@ struct Sorter {
   uint32_t gcap_hw;  // log2 of the scatter's bucket capacity
   uint32_t stride;  // ceil_log2(n) (sampler.py:121-127)
   uint32_t gs_max, smax;
+  bool no_uniq_skip = false;  // DTS_UNIQ_SKIP=0: sample children of unique-sample parents too
 
   // span / copy batches (host), flushed per level
   std::vector<Span> spans;
@@ -342,8 +343,15 @@ struct Sorter {
   // Below the root the strided subsample has <= 2^7 entries (heavy keys of
   // >= 1/128 of a segment): each sampled segment sorts its sample in one CTA.
   bool sampled_plan(uint64_t len, uint32_t remaining, uint32_t& g, uint32_t& gs, bool root,
-                    bool small_ok) const {
+                    bool small_ok, bool parent_unique = false) const {
+    // (a parent whose own sample held no repeated key — near-unique keys
+    // such as C2 — has no key frequent enough to be heavy in a child, up to
+    // the birthday test's resolution: its children skip the sample)
     const uint32_t g9 = std::min<uint32_t>(g, gcap_hw > 1 ? gcap_hw - 1 : 1);
+    if (!root && parent_unique && !no_uniq_skip) {
+      g = std::min(g9, remaining);  // (the digit a sampled plan would get: the WC scatter's)
+      return false;
+    }
     gs = std::min<uint32_t>(g9 > 1 ? g9 - 1 : 1, root ? gs_max : std::min<uint32_t>(gs_max, 7));
     uint64_t S = std::min<uint64_t>(len, (uint64_t(1) << gs) * stride);
     S = std::min<uint64_t>(S, smax);
@@ -500,7 +508,7 @@ struct Sorter {
       P.nbmax = P.nb;
       uint32_t gs = 0;
       if (dt && sampled_plan(hs.len, remaining, g, gs, (hs.root & 1u) && hs.consumed == 0,
-                             (hs.root & 2u) != 0 || segs.size() <= SAMPLE_MANY)) {
+                             (hs.root & 2u) != 0 || segs.size() <= SAMPLE_MANY, (hs.root & 4u) != 0)) {
         // sampled segments may gain heavy / overflow buckets; the digit is
         // capped so bucket ids stay below the scatter's 2^10 capacity
         P.gamma = g;
@@ -517,6 +525,10 @@ struct Sorter {
         sampled.push_back((uint32_t)i);
         hzc = std::max(hzc, (1u << g) + 1u);
         hkc = std::max(hkc, 1u << gs);
+      } else if (g != P.gamma) {  // (not sampled, digit capped for the WC scatter)
+        P.gamma = g;
+        P.shift = remaining - g;
+        P.nb = P.nbmax = 1u << g;
       }
     }
     const size_t save = meta.off;
@@ -807,11 +819,13 @@ struct Sorter {
     const uint64_t rows = std::max<uint64_t>(1, (s.len + BR - 1) / BR);
     // (the digit and bucket capacity run_wave will choose)
     uint32_t g = choose_gamma(s.len, W - s.consumed), gs = 0;
-    uint64_t nbmax = 1u << g;
+    uint64_t nbmax;
     if (cfg.mode == DTS_MODE_DT &&
         sampled_plan(s.len, W - s.consumed, g, gs, (s.root & 1u) && s.consumed == 0,
-                     (s.root & 2u) != 0 || level_segs <= SAMPLE_MANY))
+                     (s.root & 2u) != 0 || level_segs <= SAMPLE_MANY, (s.root & 4u) != 0))
       nbmax = (1u << g) + (1u << gs) + 1u;
+    else
+      nbmax = 1u << g;
     const uint64_t tiles = s.len / 2560 + rows + 1;
     return 88 + rows * 28 + nbmax * rows * 12 + (nbmax + 1) * 9 + (1u << g) * 12 + 4096 +
            tiles * (4 + ((nbmax + 1) & ~1ull) * 4);
@@ -895,6 +909,7 @@ int sort_impl(void* keys, void* vals, uint64_t n, void* ws, size_t wsb, const dt
   S.glo = (uint32_t)std::max(1, cfg->gamma_lo);
   S.stride = n <= 2 ? 1 : ceil_log2_u64(n);
   S.gs_max = sizeof(K) == 4 ? 10 : 9;
+  S.no_uniq_skip = env_int("DTS_UNIQ_SKIP", 1) == 0;
   S.smax = sizeof(K) == 4 ? 32768 : 16384;
   if (cudaEventCreateWithFlags(&S.ev_cls, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&S.ev_fork, cudaEventDisableTiming) != cudaSuccess)

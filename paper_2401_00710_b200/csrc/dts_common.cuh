@@ -15,6 +15,7 @@ enum : uint32_t {
   PF_SAMPLE = 4u,    // sample this segment on device before routing
   PF_ROOTSKIP = 8u,  // root: skip leading zero bits seen in the sample max
   PF_SPLIT = 16u,    // partition mode: route by (key, index) splitters
+  PF_UNIQ = 32u,     // the segment's sample held no repeated key (set by the sampler)
 };
 
 // Bucket kinds written for the host planner (sampler.py:103-118 descriptors)

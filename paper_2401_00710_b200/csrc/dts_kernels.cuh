@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(NT) k_sample_plan(SegPlan* __restrict__ plans,
     }
   }
   uint32_t gamma = P.gamma, shift = P.shift;
-  uint32_t flags = P.flags & ~(PF_HEAVY | PF_OVF);
+  uint32_t flags = P.flags & ~(PF_HEAVY | PF_OVF | PF_UNIQ);
   uint64_t thr = 0;
   if (flags & PF_ROOTSKIP) {
     // plan_overflow (sampler.py:192-207) at bit granularity: skip the
@@ -159,6 +159,18 @@ __global__ void __launch_bounds__(NT) k_sample_plan(SegPlan* __restrict__ plans,
       if (gamma > rem) gamma = rem;
       shift = rem - gamma;
     }
+  }
+  // no key repeats anywhere in the sorted sample (birthday test): the
+  // children of this segment skip their own samples (dts_api.cu)
+  {
+    if (threadIdx.x == 0) s_m = 0;
+    __syncthreads();
+    bool dup = false;
+    for (uint32_t i = threadIdx.x; i + 1 < S; i += NT) dup |= sm[i] == sm[i + 1];
+    if (__any_sync(FULL, dup) && (threadIdx.x & 31) == 0) s_m = 1;
+    __syncthreads();
+    if (s_m == 0) flags |= PF_UNIQ;
+    __syncthreads();
   }
   // detect_heavy (sampler.py:177-189): keys repeating in S[::stride].
   const uint32_t nsub = (uint32_t)((S + stride - 1) / stride);
@@ -433,7 +445,7 @@ __global__ void __launch_bounds__(256) k_copy_ranges(const CopyR* __restrict__ r
 // ---------------------------------------------------------------------------
 struct NextSeg {
   uint64_t offset, len;
-  uint32_t consumed, pad;  // pad: bit 0 root (host only), bit 1 parent had heavy keys
+  uint32_t consumed, pad;  // pad: bit 0 root (host only), bit 1 parent had heavy keys, bit 2 parent sample unique
 };
 
 constexpr int CLS_NT = 256;
@@ -584,8 +596,10 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(const SegPlan* __restrict__
       const uint8_t kind = kinds[P.bs_base + b];
       const uint32_t rem = kind == KIND_OVF ? W : P.shift;
       // pad bit 1: the parent segment had heavy keys (its children are
-      // sampled even when small, dts_api.cu SAMPLE_MIN)
-      next[s_base[2] + atomicAdd(&s_n[2], 1u)] = NextSeg{lo, sz, W - rem, P.nheavy ? 2u : 0u};
+      // sampled even when small, dts_api.cu SAMPLE_MIN); bit 2: the parent's
+      // sample held no repeated key (its light children are not sampled)
+      const uint32_t fl = (P.nheavy ? 2u : 0u) | ((P.flags & PF_UNIQ) && kind != KIND_OVF ? 4u : 0u);
+      next[s_base[2] + atomicAdd(&s_n[2], 1u)] = NextSeg{lo, sz, W - rem, fl};
     }
   }
 }
