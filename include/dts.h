@@ -9,7 +9,9 @@
  * (heavy_keys, heavy_lens, splitters, counts) are HOST pointers.  Every call
  * is ordered on the CUDA stream passed in and returns after the result is
  * complete on that stream (the sort reads a few per-level counters back to
- * the host, so it synchronises the stream once per MSD level).
+ * the host, so it synchronises the stream once per MSD level) — except
+ * dts_sort with dts_config.stream_ordered, which returns as soon as its last
+ * kernels are enqueued.
  *
  * Status codes: 0 ok, DTS_EINVAL (-1) invalid argument (Python: ValueError),
  * DTS_ENOMEM (-2) workspace too small (MemoryError), DTS_ECUDA (-3) CUDA
@@ -59,7 +61,11 @@ typedef struct dts_config {
   int32_t mode;                 /* DTS_MODE_DT | DTS_MODE_PLAIN                 */
   int32_t instrument;           /* fill dts_report counters                     */
   int32_t profile;              /* time every kernel with CUDA events           */
-  int32_t reserved[7];
+  int32_t stream_ordered;       /* nonzero: dts_sort returns once its last kernels
+                                   are enqueued (no final stream synchronisation;
+                                   the result is complete in stream order) —
+                                   the device-resident API (dtsort.sort_device) */
+  int32_t reserved[6];
 } dts_config;
 
 /* Mirrors InstrumentReport (core.py:167-227) plus B200 timing fields. */

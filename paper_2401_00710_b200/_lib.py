@@ -44,7 +44,8 @@ class DtsConfig(ctypes.Structure):
         ("mode", ctypes.c_int32),
         ("instrument", ctypes.c_int32),
         ("profile", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 7),
+        ("stream_ordered", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 6),
     ]
 
 

@@ -917,8 +917,15 @@ int sort_impl(void* keys, void* vals, uint64_t n, void* ws, size_t wsb, const dt
   S.side = side_stream();
   if (!S.side) return fail(DTS_ECUDA, "cudaStreamCreate failed for the classifier stream");
   int rc = S.run();
-  if (rc == 0) {
+  // (stream-ordered calls return with the last level's base case still in
+  // flight: a GPU step is not charged for the host's return path; the
+  // per-kernel timers need the stream drained)
+  if (rc == 0 && (!cfg->stream_ordered || tm.profile)) {
     cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(DTS_ECUDA, std::string("sort: ") + cudaGetErrorString(e));
+  }
+  if (rc == 0 && cfg->stream_ordered) {
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) rc = fail(DTS_ECUDA, std::string("sort: ") + cudaGetErrorString(e));
   }
   tm.harvest();

@@ -28,7 +28,7 @@ def plain_msd_sort(records: RecordArray, cfg: SortConfig | None = None) -> Instr
     return _run(records, cfg, _lib.MODE_PLAIN)
 
 
-def make_config(cfg: SortConfig, mode: int, profile: bool = False) -> _lib.DtsConfig:
+def make_config(cfg: SortConfig, mode: int, profile: bool = False, stream_ordered: bool = False) -> _lib.DtsConfig:
     if cfg.sample_rule is not None or cfg.block_policy is not None:
         raise NotImplementedError(
             "SortConfig.sample_rule / block_policy are Python callables and cannot run "
@@ -44,6 +44,7 @@ def make_config(cfg: SortConfig, mode: int, profile: bool = False) -> _lib.DtsCo
     c.mode = int(mode)
     c.instrument = int(bool(cfg.instrument))
     c.profile = int(bool(profile))
+    c.stream_ordered = int(bool(stream_ordered))
     return c
 
 
@@ -128,12 +129,14 @@ def _sort_split(keys, vals, cfg: SortConfig, mode: int, profile: bool, report: b
 
 
 def sort_device(keys, vals, cfg: SortConfig, mode: int, profile: bool = False,
-                workspace=None, report: bool = False) -> InstrumentReport | None:
+                workspace=None, report: bool = False, stream_ordered: bool = False) -> InstrumentReport | None:
     """Sort contiguous CUDA tensors in place (no validation beyond widths).
 
     ``keys``/``vals`` are torch CUDA tensors of 4/8-byte elements (any
     integer dtype of that width; bits are treated as unsigned).  Used by the
-    public sorters, the multi-GPU driver and bench.py.
+    public sorters, the multi-GPU driver and bench.py.  ``stream_ordered``:
+    return once the last kernels are enqueued (the result is complete in
+    the order of the current stream; no final host synchronisation).
     """
     torch = torch_mod()
     n = int(keys.numel())
@@ -141,7 +144,7 @@ def sort_device(keys, vals, cfg: SortConfig, mode: int, profile: bool = False,
         return _sort_split(keys, vals, cfg, mode, profile, report)
     kb = keys.element_size()
     vb = 0 if vals is None else vals.element_size()
-    c = make_config(cfg, mode, profile)
+    c = make_config(cfg, mode, profile, stream_ordered and n < split_n())
     raw = _lib.DtsReport() if (report or cfg.instrument or profile) else None
     L = _lib.lib()
     need = int(L.dts_workspace_bytes(n, kb, vb))
