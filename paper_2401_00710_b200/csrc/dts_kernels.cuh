@@ -124,21 +124,39 @@ __global__ void __launch_bounds__(NT) k_sample_plan(SegPlan* __restrict__ plans,
     }
   }
   __syncthreads();
-  // bitonic sort of sm[0..P2)
-  for (uint32_t k = 2; k <= P2; k <<= 1) {
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = threadIdx.x; i < P2 / 2; i += NT) {
-        const uint32_t a = 2 * i - (i & (j - 1));
-        const uint32_t b = a + j;
-        const bool up = (a & k) == 0;
-        const K x = sm[a], y = sm[b];
-        if ((x > y) == up) {
-          sm[a] = y;
-          sm[b] = x;
+  // bitonic sort of sm[0..P2).  Stages with compare distance j <= 128 stay
+  // inside aligned 256-element blocks: warp w owns blocks w, w + NW, ... (its
+  // lanes take the block's 128 pairs), so those stages need only __syncwarp;
+  // a block barrier is needed only around the j >= 256 stages (8192 keys:
+  // 20 block barriers instead of 91).
+  {
+    constexpr uint32_t NWS = NT / 32;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t nblk = (P2 + 255) / 256;
+    auto cswap = [&](uint32_t a, uint32_t j, uint32_t k) {
+      const uint32_t b = a + j;
+      const bool up = (a & k) == 0;
+      const K x = sm[a], y = sm[b];
+      if ((x > y) == up) {
+        sm[a] = y;
+        sm[b] = x;
+      }
+    };
+    for (uint32_t k = 2; k <= P2; k <<= 1) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        if (j >= 256) {
+          for (uint32_t i = threadIdx.x; i < P2 / 2; i += NT) cswap(2 * i - (i & (j - 1)), j, k);
+          __syncthreads();
+        } else {
+          const uint32_t np = P2 < 256 ? P2 / 2 : 128u;  // pairs per block
+          for (uint32_t bl = warp; bl < nblk; bl += NWS)
+            for (uint32_t r = lane; r < np; r += 32) cswap(256 * bl + 2 * r - (r & (j - 1)), j, k);
+          __syncwarp();
         }
       }
-      __syncthreads();
+      if (k >= 256) __syncthreads();  // (the next k starts with a block-wide stage)
     }
+    __syncthreads();
   }
   uint32_t gamma = P.gamma, shift = P.shift;
   uint32_t flags = P.flags & ~(PF_HEAVY | PF_OVF | PF_UNIQ);
