@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/dts.h"
@@ -115,17 +116,30 @@ struct Pinned {
 thread_local Pinned g_pin_plan, g_pin_back, g_pin_span;
 
 // Per-thread, per-device side stream (high priority, non-blocking) for the
-// classifier; created once and kept (a stream per call would cost ~10 us).
-cudaStream_t side_stream() {
-  static thread_local cudaStream_t streams[64] = {};
+// classifier and the sorter's two fork / join events; created once and kept
+// (creating them per call costs host microseconds at the start of a sort).
+cudaStream_t side_stream(cudaEvent_t* ev_cls, cudaEvent_t* ev_fork) {
+  struct Side {
+    cudaStream_t st = nullptr;
+    cudaEvent_t cls = nullptr, fork = nullptr;
+  };
+  static thread_local Side sides[64];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  if (!streams[dev]) {
+  Side& s = sides[dev];
+  if (!s.st) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    if (cudaStreamCreateWithPriority(&streams[dev], cudaStreamNonBlocking, hi) != cudaSuccess) return nullptr;
+    if (cudaStreamCreateWithPriority(&s.st, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s.cls, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming) != cudaSuccess) {
+      s.st = nullptr;
+      return nullptr;
+    }
   }
-  return streams[dev];
+  *ev_cls = s.cls;
+  *ev_fork = s.fork;
+  return s.st;
 }
 
 int device_sms() {
@@ -214,21 +228,53 @@ struct Timer {
   }
 };
 
+// Kernel attributes and occupancies are set / queried once per (thread,
+// device, kernel, size) and cached: each driver call costs microseconds of
+// host time that the GPU spends idle at the start of a level.
+struct AttrKey {
+  const void* fn;
+  int dev, nt;
+  size_t bytes;
+  bool operator==(const AttrKey& o) const { return fn == o.fn && dev == o.dev && nt == o.nt && bytes == o.bytes; }
+};
+struct AttrHash {
+  size_t operator()(const AttrKey& k) const {
+    return std::hash<const void*>()(k.fn) ^ (std::hash<size_t>()(k.bytes) * 31u) ^ (size_t)(k.dev * 131 + k.nt);
+  }
+};
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
 template <typename F>
 int set_smem(F* fn, size_t bytes) {
   if (bytes > 48 * 1024) {
+    static thread_local std::unordered_map<AttrKey, int, AttrHash> done;
+    const AttrKey key{(const void*)fn, current_device(), 0, bytes};
+    if (done.count(key)) return 0;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess)
       return fail(DTS_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    done.emplace(key, 1);
   }
   return 0;
 }
 
 template <typename F>
 int persistent_grid(F* fn, int nt, size_t smem, uint32_t nblk) {
+  static thread_local std::unordered_map<AttrKey, int, AttrHash> occ;
+  const AttrKey key{(const void*)fn, current_device(), nt, smem};
+  auto it = occ.find(key);
   int per = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, nt, smem);
-  if (per < 1) per = 1;
+  if (it != occ.end()) {
+    per = it->second;
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, nt, smem);
+    if (per < 1) per = 1;
+    occ.emplace(key, per);
+  }
   const uint64_t g = (uint64_t)per * device_sms();
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(g, nblk));
 }
@@ -911,11 +957,8 @@ int sort_impl(void* keys, void* vals, uint64_t n, void* ws, size_t wsb, const dt
   S.gs_max = sizeof(K) == 4 ? 10 : 9;
   S.no_uniq_skip = env_int("DTS_UNIQ_SKIP", 1) == 0;
   S.smax = sizeof(K) == 4 ? 32768 : 16384;
-  if (cudaEventCreateWithFlags(&S.ev_cls, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&S.ev_fork, cudaEventDisableTiming) != cudaSuccess)
-    return fail(DTS_ECUDA, "cudaEventCreate failed");
-  S.side = side_stream();
-  if (!S.side) return fail(DTS_ECUDA, "cudaStreamCreate failed for the classifier stream");
+  S.side = side_stream(&S.ev_cls, &S.ev_fork);
+  if (!S.side) return fail(DTS_ECUDA, "cudaStreamCreate / cudaEventCreate failed for the classifier stream");
   int rc = S.run();
   // (stream-ordered calls return with the last level's base case still in
   // flight: a GPU step is not charged for the host's return path; the
@@ -930,8 +973,6 @@ int sort_impl(void* keys, void* vals, uint64_t n, void* ws, size_t wsb, const dt
   }
   tm.harvest();
   if (rc != 0) cudaStreamSynchronize(S.side);  // (nothing of this call left in flight)
-  cudaEventDestroy(S.ev_cls);
-  cudaEventDestroy(S.ev_fork);
   if (rep) rep->gpu_launches += tm.launches;
   return rc;
 }
