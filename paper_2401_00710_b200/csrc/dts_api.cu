@@ -115,6 +115,31 @@ struct Pinned {
 };
 thread_local Pinned g_pin_plan, g_pin_back, g_pin_span;
 
+// Mapped pinned host memory (zero-copy): k_classify writes the next level's
+// segment list straight into it, so the host has the whole list when the
+// classifier's event fires — whatever its length, without a copy that
+// would queue behind the scatter.
+struct Mapped {
+  void* p = nullptr;
+  void* d = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return 0;
+    if (p) cudaFreeHost(p);
+    p = d = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 1 << 20);
+    want = want + want / 2;
+    if (cudaHostAlloc(&p, want, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+      return fail(DTS_ECUDA, "cudaHostAlloc (mapped) failed for the next-segment list");
+    if (cudaHostGetDevicePointer(&d, p, 0) != cudaSuccess)
+      return fail(DTS_ECUDA, "cudaHostGetDevicePointer failed for the next-segment list");
+    cap = want;
+    return 0;
+  }
+};
+thread_local Mapped g_map_next;
+
 // Per-thread, per-device side stream (high priority, non-blocking) for the
 // classifier and the sorter's two fork / join events; created once and kept
 // (creating them per call costs host microseconds at the start of a sort).
@@ -749,9 +774,10 @@ struct Sorter {
     const uint64_t cap_copy = bs_total + wave_recs / COPY_CHUNK + 1;
     Span* dspan = (Span*)meta.take(std::max<uint64_t>(1, bs_total) * sizeof(Span));
     CopyR* dcopy = (CopyR*)meta.take(cap_copy * sizeof(CopyR));
-    NextSeg* dnext = (NextSeg*)meta.take(std::max<uint64_t>(1, bs_total) * sizeof(NextSeg));
+    DTS_TRY(g_map_next.ensure(std::max<uint64_t>(1, bs_total) * sizeof(NextSeg)));
+    NextSeg* dnext = (NextSeg*)g_map_next.d;  // (mapped host memory)
     unsigned long long* dcc = (unsigned long long*)meta.take(8 * sizeof(unsigned long long));
-    if (!dspan || !dcopy || !dnext || !dcc) return fail(DTS_ENOMEM, "workspace too small for level metadata");
+    if (!dspan || !dcopy || !dcc) return fail(DTS_ENOMEM, "workspace too small for level metadata");
     // (on the side stream: the classifier's few CTAs and the read-back run
     // beside the scatter, which only needs the scan; the base case waits)
     // Only before the write-combining scatter (stripes taken in any order):
@@ -768,14 +794,10 @@ struct Sorter {
                                              dspan, dcopy, dnext, dcc);
     tm.launches += 1;
     DTS_TRY(check_launch("k_classify"));
-    constexpr uint64_t NEXT_CAP = 4096;  // next segments returned with the counters
-    const uint64_t ncap = std::min<uint64_t>(NEXT_CAP, std::max<uint64_t>(1, bs_total));
-    DTS_TRY(g_pin_back.ensure(256 + align256(pb) + ncap * sizeof(NextSeg) + 256));
+    DTS_TRY(g_pin_back.ensure(256 + align256(pb) + 256));
     char* bp = (char*)g_pin_back.p;
     CUDA_TRY(cudaMemcpyAsync(bp, dcc, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs));
     CUDA_TRY(cudaMemcpyAsync(bp + 256, dplans, pb, cudaMemcpyDeviceToHost, cs));
-    CUDA_TRY(cudaMemcpyAsync(bp + 256 + align256(pb), dnext, ncap * sizeof(NextSeg),
-                             cudaMemcpyDeviceToHost, cs));
     CUDA_TRY(cudaEventRecord(ev_cls, cs));
     // ---- scatter (after the classifier: it only needs the bucket bounds,
     // so the host receives the next level while the scatter runs) ----
@@ -826,14 +848,7 @@ struct Sorter {
     // NextSeg.pad = 0 reads as root = false)
     const size_t nx0 = next.size();
     next.resize(nx0 + nnx);
-    if (nnx <= ncap) {
-      if (nnx) std::memcpy(next.data() + nx0, bp + 256 + align256(pb), nnx * sizeof(NextSeg));
-    } else {
-      // (more next segments than the pinned back-buffer holds: C4's deep
-      // levels) — read on the side stream, which the classifier ran on
-      CUDA_TRY(cudaMemcpyAsync(next.data() + nx0, dnext, nnx * sizeof(NextSeg), cudaMemcpyDeviceToHost, cs));
-      CUDA_TRY(cudaStreamSynchronize(cs));
-    }
+    if (nnx) std::memcpy(next.data() + nx0, g_map_next.p, nnx * sizeof(NextSeg));
     if (rep) {
       rep->moves += wave_recs + hc[6] + hc[7];
       rep->records_distributed += wave_recs;
