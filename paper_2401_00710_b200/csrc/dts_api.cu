@@ -603,6 +603,7 @@ struct Sorter {
       }
     }
     const size_t save = meta.off;
+    const double t_p1 = trace_on() ? now_us() : 0.0;
     const size_t pb = ns * sizeof(SegPlan), sb = sampled.size() * 4;
     SegPlan* dplans = (SegPlan*)meta.take(pb);
     uint32_t* dsampled = (uint32_t*)meta.take(std::max<size_t>(1, sampled.size()) * 4);
@@ -652,6 +653,7 @@ struct Sorter {
     static const uint64_t wc_lbs = (uint64_t)std::max(1, env_int("DTS_WC_LBS", (int)WC_LBS));
     const uint64_t BR = wc ? (uint64_t)WcTile<K, VB>::T * wc_lbs : block_records(sizeof(K), VB);
     const uint64_t TT = wc ? (uint64_t)WcTile<K, VB>::T : (uint64_t)ScatterTile<K, VB>::T;
+    const double t_p2 = trace_on() ? now_us() : 0.0;
     // ---- count-matrix shape and hist blocks ----
     std::vector<Blk> blks;
     blks.reserve(ns + wave_recs / BR + 1);
@@ -696,6 +698,7 @@ struct Sorter {
       }
     }
 
+    const double t_p3 = trace_on() ? now_us() : 0.0;
     // ---- device meta ----
     Blk* dblks = (Blk*)meta.take(blks.size() * sizeof(Blk));
     uint32_t* dcnt = (uint32_t*)meta.take(cnt_total * 4);
@@ -744,6 +747,7 @@ struct Sorter {
       tm.end(ev, sampled.size());
       DTS_TRY(check_launch("k_sample_plan"));
     }
+    const double t_p4 = trace_on() ? now_us() : 0.0;
     // ---- histogram ----
     {
       CUDA_TRY(cudaMemsetAsync(dctr, 0, 16, st));
@@ -871,6 +875,8 @@ struct Sorter {
                    sampled.size(), (int)wc, nbc, t_launch - t_plan0, t_sync - t_launch,
                    (unsigned long long)nsp, (unsigned long long)ncp, (unsigned long long)nnx,
                    now_us() - t_sync);
+      std::fprintf(stderr, "[dts]   host: segment plans %.0f us, sample + read-back %.0f us, blocks / tile lists %.0f us, "
+                   "meta + H2D %.0f us\n", t_p1 - t_plan0, t_p2 - t_p1, t_p3 - t_p2, t_p4 - t_p3);
     }
     return 0;
   }
@@ -907,11 +913,15 @@ struct Sorter {
     while (!segs.empty()) {
       std::vector<HostSeg> next;
       size_t s0 = 0;
+      // (waves of at most wave_segs segments: the host plans wave k + 1
+      // while the GPU runs wave k — a level of 10^5 small segments, C4's
+      // third, costs milliseconds of host planning)
+      static const size_t wave_segs = (size_t)std::max(1, env_int("DTS_WAVE_SEGS", 1 << 30));
       while (s0 < segs.size()) {
         size_t s1 = s0, need = 1 << 16;
         while (s1 < segs.size()) {
           const size_t b = wave_meta_bytes(segs[s1], segs.size());
-          if (s1 > s0 && need + b > budget) break;
+          if (s1 > s0 && (need + b > budget || s1 - s0 >= wave_segs)) break;
           need += b;
           ++s1;
         }

@@ -10,7 +10,8 @@ namespace dts {
 #endif
 
 #ifndef DTS_OVN_LSD
-#define DTS_OVN_LSD 16 // wrapped 4-bit fields in one warp that send a span to LSD, not the retry
+#define DTS_OVN_LSD (1 << 30)  // wrapped 4-bit fields in one warp that send a span to LSD, not the retry
+                               // (the retry's 16-bit fields cannot carry: every carrying span is queued)
 #endif
 
 template <int FB> struct FieldBits {
@@ -280,11 +281,14 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
           if constexpr (FB == 4) {
             x = (x & 0x0F0F0F0Fu) + ((x >> 4) & 0x0F0F0F0Fu);
             return (x * 0x01010101u) >> 24;
-          } else {
+          } else if constexpr (FB == 8) {
             return __dp4a(x, 0x01010101u, 0u);
+          } else {
+            return (x & 0xFFFFu) + (x >> 16);
           }
         };
-        const uint32_t nib = FB == 4 ? 4u * (uint32_t)warp : 8u * ((uint32_t)warp >> 1);
+        const uint32_t nib = FB == 4 ? 4u * (uint32_t)warp
+                                     : (FB == 8 ? 8u * ((uint32_t)warp >> 1) : 16u * ((uint32_t)warp >> 2));
         uint32_t rkp[(IPT + RPW - 1) / RPW];  // own-group ranks, FB bits each
 #pragma unroll
         for (int j = 0; j < (IPT + RPW - 1) / RPW; ++j) rkp[j] = 0u;
@@ -312,10 +316,19 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
         };
         if constexpr (FB == 4) {
           atomics();
-        } else {
+        } else if constexpr (FB == 8) {
           if (!(warp & 1)) atomics();
           __syncthreads();
           if (warp & 1) atomics();
+        } else {
+          // 16-bit fields, 2 groups of 4 warps whose atomics run in 4 phases
+          // (warp order inside a group): no field can carry (spans hold
+          // < 2^16 records), so a span never needs the LSD passes
+#pragma unroll 1
+          for (int ph = 0; ph < 4; ++ph) {
+            if ((warp & 3) == ph) atomics();
+            if (ph < 3) __syncthreads();
+          }
         }
         if (ovf) s_big = 1u;  // a field would carry
         __syncthreads();
@@ -447,6 +460,13 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
 #endif
       if constexpr (RETRY) {
         if (counting(FieldBits<8>{})) continue;
+        // a byte field would carry (a key with hundreds of copies per warp
+        // pair): bins back to zero, then 16-bit fields — never LSD
+        for (uint32_t q = tid; q < nq; q += NT) reinterpret_cast<uint4*>(cnt)[q] = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+        if (tid == 0) s_big = 0u;
+        __syncthreads();
+        if (counting(FieldBits<16>{})) continue;
       } else {
         if (counting(FieldBits<4>{})) continue;
         if (rq != nullptr) {
