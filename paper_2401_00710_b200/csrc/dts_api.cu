@@ -10,6 +10,7 @@
 // reference's.
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -650,26 +651,60 @@ struct Sorter {
     }
     nbc = (nbc + 1) & ~1u;
     const bool wc = wc_env != 0 && nbc <= (uint32_t)WcTile<K, VB>::NBW;
-    static const uint64_t wc_lbs = (uint64_t)std::max(1, env_int("DTS_WC_LBS", (int)WC_LBS));
+    static const int wc_lbs_env = env_int("DTS_WC_LBS", 0);
+    const uint64_t wc_lbs = wc_lbs_env > 0 ? (uint64_t)wc_lbs_env : WC_LBS;
     const uint64_t BR = wc ? (uint64_t)WcTile<K, VB>::T * wc_lbs : block_records(sizeof(K), VB);
     const uint64_t TT = wc ? (uint64_t)WcTile<K, VB>::T : (uint64_t)ScatterTile<K, VB>::T;
     const double t_p2 = trace_on() ? now_us() : 0.0;
     // ---- count-matrix shape and hist blocks ----
+    // Stripes (WC) go to one persistent CTA per SM in order: the wave gets
+    // a multiple of the CTA count of about WC_LBS tiles each, shared out
+    // over its segments in proportion to their length (largest remainders),
+    // so the last round of stripes keeps every SM busy (C2 level 0: 44-tile
+    // stripes gave 3171 = 21 x 148 + 63 — 85 SMs idle for the last stripe).
+    std::vector<uint64_t> seg_rows(ns);
+    if (wc && wc_lbs_env <= 0) {
+      const uint64_t G = (uint64_t)device_sms();
+      uint64_t total_tiles = 0;
+      for (size_t i = 0; i < ns; ++i) total_tiles += (plans[i].len + TT - 1) / TT;
+      const uint64_t k = std::max<uint64_t>(1, (total_tiles + G * WC_LBS / 2) / (G * WC_LBS));
+      const uint64_t R = std::max<uint64_t>(G * k, 1);
+      std::vector<std::pair<double, size_t>> frac;
+      uint64_t given = 0;
+      for (size_t i = 0; i < ns; ++i) {
+        const double want = (double)plans[i].len * (double)R / (double)std::max<uint64_t>(wave_recs, 1);
+        const uint64_t tiles = std::max<uint64_t>(1, (plans[i].len + TT - 1) / TT);
+        seg_rows[i] = std::min<uint64_t>(tiles, std::max<uint64_t>(1, (uint64_t)want));
+        given += seg_rows[i];
+        if (seg_rows[i] < tiles) frac.emplace_back(want - std::floor(want), i);
+      }
+      if (given < R) {
+        const size_t extra = std::min<size_t>(frac.size(), (size_t)(R - given));
+        std::partial_sort(frac.begin(), frac.begin() + extra, frac.end(),
+                          [](const std::pair<double, size_t>& x, const std::pair<double, size_t>& y) {
+                            return x.first > y.first;
+                          });
+        for (size_t j = 0; j < extra; ++j) ++seg_rows[frac[j].second];
+      }
+    } else {
+      for (size_t i = 0; i < ns; ++i) seg_rows[i] = std::max<uint64_t>(1, (plans[i].len + BR - 1) / BR);
+    }
     std::vector<Blk> blks;
     blks.reserve(ns + wave_recs / BR + 1);
     uint64_t cnt_total = 0, bs_total = 0;
     for (size_t i = 0; i < ns; ++i) {
       SegPlan& P = plans[i];
       const uint64_t len = P.len;
-      const uint64_t rows = std::max<uint64_t>(1, (len + BR - 1) / BR);
+      // whole tiles per block, no empty blocks
+      const uint64_t per0 = ((len + seg_rows[i] - 1) / seg_rows[i] + TT - 1) / TT * TT;
+      const uint64_t rows = std::max<uint64_t>(1, (len + per0 - 1) / per0);
       if (wc_env && (P.flags & PF_SAMPLE)) P.nbmax = P.nb;  // resolved
       P.nrows = (uint32_t)rows;
       P.cnt_base = cnt_total;
       cnt_total += (uint64_t)P.nbmax * rows;
       P.bs_base = (uint32_t)bs_total;
       bs_total += P.nbmax + 1;
-      // whole tiles per block
-      const uint64_t per = ((len + rows - 1) / rows + TT - 1) / TT * TT;
+      const uint64_t per = per0;
       for (uint64_t r = 0; r < rows; ++r) {
         Blk b;
         b.seg = (uint32_t)i;
