@@ -80,16 +80,41 @@ def gen_device(cfg, n, seed, device, gbase=0):
 # clocks sampler (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------
 class Clocks:
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    every 1 ms from a thread (a region of a few ms still gets samples), else
+    nvidia-smi every 20 ms."""
+
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, gpu_index: int):
-        self.idx = gpu_index
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [x.strip() for x in vis.split(",") if x.strip()]
+        self.idx = int(ids[gpu_index]) if gpu_index < len(ids) and ids[gpu_index].isdigit() else gpu_index
         self.proc = None
+        self.nvml = None
         self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
+        self.stop_ev = threading.Event()
 
     def start(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            self.nvml = (pynvml, h)
+            self.bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                         "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                         "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                         "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -99,28 +124,49 @@ class Clocks:
         except Exception:
             self.proc = None
 
+    def _poll(self):
+        nv, h = self.nvml
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx,
+                                     nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+            except Exception:
+                pass
+            time.sleep(0.001)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def wait_first(self, timeout_s: float = 5.0):
-        """Block until nvidia-smi has produced its first sample (its start-up
-        can outlast a short timed region)."""
+        """Block until the sampler has produced its first sample (nvidia-smi's
+        start-up can outlast a short timed region); keep only later samples."""
         t0 = time.time()
-        while self.proc is not None and not self.lines and time.time() - t0 < timeout_s:
-            time.sleep(0.01)
-        self.lines.clear()  # keep only samples taken from here on
+        while (self.proc is not None and not self.lines) or (self.nvml is not None and not self.samples):
+            if time.time() - t0 > timeout_s:
+                break
+            time.sleep(0.001)
+        self.lines.clear()
+        self.samples.clear()
 
     def stop(self):
+        if self.nvml is not None:
+            self.stop_ev.set()
+            self.t.join(timeout=2)
+            sm = [x[0] for x in self.samples]
+            reasons = sorted(nm for nm, bit in self.bits.items() if any(x[2] & bit for x in self.samples))
+            return {"sm_mhz": float(np.median(sm)) if sm else None,
+                    "sm_max_mhz": float(self.samples[0][1]) if self.samples else None,
+                    "reasons": reasons, "samples": len(sm), "source": "nvml, 1 ms"}
         if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampler unavailable"]}
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
@@ -130,11 +176,11 @@ class Clocks:
                 mx = float(f[2])
             except ValueError:
                 continue
-            for nm, v in zip(names, f[5:9]):
+            for nm, v in zip(self.NAMES, f[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi, 20 ms"}
 
 
 # ---------------------------------------------------------------------------
