@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
   __syncthreads();
   uint32_t ph0 = 0u, ph1 = 0u;
   int cur = 0;
-  constexpr bool ph_on = DTS_PHASE_PROF == 2;
+  [[maybe_unused]] constexpr bool ph_on = DTS_PHASE_PROF == 2;
   PH_INIT
   for (uint32_t sidx = blockIdx.x; sidx < nspan; sidx += G, cur ^= 1) {
     PH(9)
@@ -661,7 +661,6 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
       __syncthreads();
       if (s_fix || DTS_FORCE_FIXUP) {
         for (uint32_t p = tid; p < n; p += NT) {
-          const uint32_t x = si[p];
           const uint32_t dx = (uint32_t)(sk[p] >> sh) & (D - 1);
           auto same = [&](uint32_t q) { return ((uint32_t)(sk[q] >> sh) & (D - 1)) == dx; };
           const bool leader = p == 0 || !same(p - 1);

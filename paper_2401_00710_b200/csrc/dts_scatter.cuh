@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
   __syncthreads();
   uint32_t phase = 0u;
   int cur = 0;
-  constexpr bool ph_on = DTS_PHASE_PROF == 1;
+  [[maybe_unused]] constexpr bool ph_on = DTS_PHASE_PROF == 1;
   PH_INIT
 
   for (uint32_t t = blockIdx.x; t < ntile; t += gridDim.x, cur ^= 1) {

@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
   for (uint32_t i = tid; i < NW * HW; i += NT) wh[i] = 0u;
   uint32_t ph0 = 0u, ph1 = 0u;
   int cur = 0;
-  constexpr bool ph_on = DTS_PHASE_PROF == 1;
+  [[maybe_unused]] constexpr bool ph_on = DTS_PHASE_PROF == 1;
   PH_INIT
 
   // thread 0: stream records [g0, g0+tn) into buffer b

@@ -8,9 +8,12 @@ follow the reference's structure when SortConfig(instrument=True): the
 reference digit policy (core.py:154-164), its base-case threshold
 (core.py:148-151), the root's gamma-granular leading-digit skip
 (sampler.py:192-207) and its `moves` accounting (dtsort.py:64-108).
-The sample draws are a counter-based hash, not numpy's Philox, so the
-statistical assertions (heavy detection, skip on a lucky sample) hold while
-exact counter equality with the reference is not claimed.
+The report is the host replay of the reference recursion
+(paper_2401_00710_b200/replay.py) over the GPU's stable (key, index) sort,
+drawing the reference's own numpy Philox sample streams, so the counters
+equal the reference's value for value (pinned on the 99 golden reports in
+tests/test_replay_golden.py and through the GPU at the end of this file);
+the GPU pipeline's own structure is checked in tests/test_gpu_structure.py.
 """
 import numpy as np
 import pytest
