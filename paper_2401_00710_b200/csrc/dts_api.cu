@@ -632,7 +632,7 @@ struct Sorter {
       DTS_TRY(set_smem(fn, sm));
       fn<<<(unsigned)sampled.size(), SAMPLE_NT, sm, st>>>(dplans, dsampled, ink, dheavy, dhz,
                                                            cfg.seed, (uint32_t)level, stride,
-                                                           gs_max, smax);
+                                                           gs_max, smax, (uint32_t)WcTile<K, VB>::NBW);
       tm.end(ev, sampled.size());
       DTS_TRY(check_launch("k_sample_plan"));
       if (wc_env) {
@@ -778,7 +778,7 @@ struct Sorter {
                                cudaMemcpyHostToDevice, st));
       fn<<<(unsigned)sampled.size(), SAMPLE_NT, sm, st>>>(dplans, dsampled, ink, dheavy, dhz,
                                                            cfg.seed, (uint32_t)level, stride,
-                                                           gs_max, smax);
+                                                           gs_max, smax, (uint32_t)WcTile<K, VB>::NBW);
       tm.end(ev, sampled.size());
       DTS_TRY(check_launch("k_sample_plan"));
     }
