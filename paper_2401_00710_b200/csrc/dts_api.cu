@@ -618,6 +618,10 @@ struct Sorter {
     // so the scatter variant and the count-matrix shape fit the real bucket
     // counts ----
     static const int wc_env = env_int("DTS_WC", 1);
+    static const int wide_env = env_int("DTS_WC_WIDE", 1);
+    // sampler: the columns of the write-combining scatter | its wide variant's << 16
+    const uint32_t wc_cols =
+        (uint32_t)WcTile<K, VB>::NBW | (wide_env ? (uint32_t)WcTile<K, VB, 1>::NBW << 16 : 0u);
     if (!sampled.empty()) {
       DTS_TRY(g_pin_plan.ensure(align256(pb) + sb + 512));
       char* hp = (char*)g_pin_plan.p;
@@ -632,7 +636,7 @@ struct Sorter {
       DTS_TRY(set_smem(fn, sm));
       fn<<<(unsigned)sampled.size(), SAMPLE_NT, sm, st>>>(dplans, dsampled, ink, dheavy, dhz,
                                                            cfg.seed, (uint32_t)level, stride,
-                                                           gs_max, smax, (uint32_t)WcTile<K, VB>::NBW);
+                                                           gs_max, smax, wc_cols);
       tm.end(ev, sampled.size());
       DTS_TRY(check_launch("k_sample_plan"));
       if (wc_env) {
@@ -650,11 +654,14 @@ struct Sorter {
       nbc = std::max(nbc, known ? plans[i].nb : plans[i].nbmax);
     }
     nbc = (nbc + 1) & ~1u;
-    const bool wc = wc_env != 0 && nbc <= (uint32_t)WcTile<K, VB>::NBW;
+    // (the wide variant takes heavy-key-rich waves of up to 600 columns)
+    const bool wc = wc_env != 0 && nbc <= (wide_env ? (uint32_t)WcTile<K, VB, 1>::NBW : (uint32_t)WcTile<K, VB>::NBW);
+    const bool wide = wc && nbc > (uint32_t)WcTile<K, VB>::NBW;
+    const uint64_t WT = wide ? (uint64_t)WcTile<K, VB, 1>::T : (uint64_t)WcTile<K, VB>::T;
     static const int wc_lbs_env = env_int("DTS_WC_LBS", 0);
     const uint64_t wc_lbs = wc_lbs_env > 0 ? (uint64_t)wc_lbs_env : WC_LBS;
-    const uint64_t BR = wc ? (uint64_t)WcTile<K, VB>::T * wc_lbs : block_records(sizeof(K), VB);
-    const uint64_t TT = wc ? (uint64_t)WcTile<K, VB>::T : (uint64_t)ScatterTile<K, VB>::T;
+    const uint64_t BR = wc ? WT * wc_lbs : block_records(sizeof(K), VB);
+    const uint64_t TT = wc ? WT : (uint64_t)ScatterTile<K, VB>::T;
     const double t_p2 = trace_on() ? now_us() : 0.0;
     // ---- count-matrix shape and hist blocks ----
     // Stripes (WC) go to one persistent CTA per SM in order: the wave gets
@@ -778,7 +785,7 @@ struct Sorter {
                                cudaMemcpyHostToDevice, st));
       fn<<<(unsigned)sampled.size(), SAMPLE_NT, sm, st>>>(dplans, dsampled, ink, dheavy, dhz,
                                                            cfg.seed, (uint32_t)level, stride,
-                                                           gs_max, smax, (uint32_t)WcTile<K, VB>::NBW);
+                                                           gs_max, smax, wc_cols);
       tm.end(ev, sampled.size());
       DTS_TRY(check_launch("k_sample_plan"));
     }
@@ -844,8 +851,8 @@ struct Sorter {
       CUDA_TRY(cudaMemsetAsync(dctr + 1, 0, 4, st));
       Timer::Ev ev;
       tm.begin(DTS_K_SCATTER, ev);
-      auto fn = k_scatter_wc<K, VB>;
-      const size_t sm = WcSmem<K, VB>::total;
+      auto fn = wide ? k_scatter_wc<K, VB, 1> : k_scatter_wc<K, VB, 0>;
+      const size_t sm = wide ? WcSmem<K, VB, 1>::total : WcSmem<K, VB, 0>::total;
       DTS_TRY(set_smem(fn, sm));
       const int grid = persistent_grid(fn, WcTile<K, VB>::NT, sm, (uint32_t)blks.size());
       fn<<<grid, WcTile<K, VB>::NT, sm, st>>>(dplans, dblks, (uint32_t)blks.size(), dctr + 1, ink, inv,

@@ -166,28 +166,53 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 // zone, with heavy keys splitting their zone's light bucket so every bucket
 // id is monotone in the key (sampler.py:76-100 precedence; the id layout is
 // the fused-dovetail layout of DESIGN.md §4).
+//
+// The SMEM zone table is packed: hzp[z] = base(z) | (heavy keys in zone z)
+// << 16, base(z) = z + 2 * #heavy keys below zone z (hz_pool holds the
+// plain prefix counts; `pack_zone_table` converts).  A key of a zone with at
+// most one heavy key is routed without a branch (the zone's first heavy key
+// is loaded unconditionally and compared); only zones holding several heavy
+// keys search the rest.  (A divergent binary search on every zone that holds
+// a heavy key made every warp instruction of a Zipf input take the slow
+// path: 1.6 warp instructions per record in k_histogram, 5x C2's.)
 template <typename K>
 struct Router {
   K ovf_thr;
   uint32_t shift, mask, flags, nb;
-  const uint32_t* hz;
+  const uint32_t* hz;  // packed zone table
   const K* hk;
 
   __device__ __forceinline__ uint32_t operator()(K key) const {
-    if ((flags & PF_OVF) && key >= ovf_thr) return nb - 1;
     const uint32_t z = (uint32_t)(key >> shift) & mask;
-    if (!(flags & PF_HEAVY)) return z;
-    const uint32_t h0 = hz[z], h1 = hz[z + 1];
-    const uint32_t base = z + 2u * h0;
-    if (h0 == h1) return base;
-    uint32_t lo = h0, hi = h1;
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (hk[mid] < key) lo = mid + 1; else hi = mid;
+    uint32_t b = z;
+    if (flags & PF_HEAVY) {
+      const uint32_t e = hz[z];
+      const uint32_t c = e >> 16;
+      b = e & 0xffffu;
+      const uint32_t h0 = (b - z) >> 1;
+      const K x = hk[c ? h0 : 0u];
+      b += (c != 0u && x <= key) ? (x == key ? 1u : 2u) : 0u;
+      if (c > 1u && x < key) {  // several heavy keys in the zone (rare)
+        uint32_t lo = h0 + 1, hi = h0 + c;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (hk[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        b = (e & 0xffffu) + 2u * (lo - h0) + ((lo < h0 + c && hk[lo] == key) ? 1u : 0u);
+      }
     }
-    return base + 2u * (lo - h0) + ((lo < h1 && hk[lo] == key) ? 1u : 0u);
+    return ((flags & PF_OVF) && key >= ovf_thr) ? nb - 1 : b;
   }
 };
+
+// SMEM packed zone table from the prefix counts (nz = 2^gamma zones).
+__device__ __forceinline__ void pack_zone_table(const uint32_t* __restrict__ hzc, uint32_t nz,
+                                                uint32_t* hzp) {
+  for (uint32_t z = threadIdx.x; z < nz; z += blockDim.x) {
+    const uint32_t h0 = hzc[z], h1 = hzc[z + 1];
+    hzp[z] = (z + 2u * h0) | ((h1 - h0) << 16);
+  }
+}
 
 // Partition router: destination = number of (key, index) splitters strictly
 // below the record (SURVEY.md §8e composite splitters).

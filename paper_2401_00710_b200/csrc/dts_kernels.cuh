@@ -63,8 +63,7 @@ __device__ __forceinline__ void load_tables(const SegPlan& P, const K* __restric
       }
     }
   } else if (P.flags & PF_HEAVY) {
-    const uint32_t nz = (1u << P.gamma) + 1u;
-    for (uint32_t i = threadIdx.x; i < nz; i += blockDim.x) hz[i] = hz_pool[P.hz_base + i];
+    pack_zone_table(hz_pool + P.hz_base, 1u << P.gamma, hz);
     for (uint32_t i = threadIdx.x; i < P.nheavy; i += blockDim.x)
       hk[i] = heavy_pool[P.heavy_base + i];
   }
@@ -231,9 +230,13 @@ __global__ void __launch_bounds__(NT) k_sample_plan(SegPlan* __restrict__ plans,
   // output).  Kept keys are the ones with the most subsample hits, in key
   // order.  (Zipf 1.0: 8 qualify at the root, the 5 lightest hold ~3.6 %:
   // WC; Zipf 1.5 / 1.2: the keys beyond 3 hold 11-15 %: all kept.)
+  // (wc_cols = the write-combining scatter's columns | its wide variant's
+  // columns << 16: the wide variant is the second choice)
   const uint32_t m_all = (P.nbmax - (1u << gamma) - 1u) / 2u;
   const uint32_t ovf1 = (flags & PF_OVF) ? 1u : 0u;
-  const uint32_t m_wc = wc_cols > (1u << gamma) + ovf1 ? (wc_cols - (1u << gamma) - ovf1) / 2u : 0u;
+  const uint32_t wc1 = wc_cols & 0xffffu, wc2 = wc_cols >> 16;
+  const uint32_t m_wc = wc1 > (1u << gamma) + ovf1 ? (wc1 - (1u << gamma) - ovf1) / 2u : 0u;
+  const uint32_t m_wc2 = wc2 > (1u << gamma) + ovf1 ? (wc2 - (1u << gamma) - ovf1) / 2u : 0u;
   __syncthreads();
   uint32_t m = min(s_m, m_all);
   if (s_m > m_wc) {
@@ -255,10 +258,11 @@ __global__ void __launch_bounds__(NT) k_sample_plan(SegPlan* __restrict__ plans,
       }
       s_hc[c] = lo2 - lo;
     }
-    __shared__ uint32_t s_drop;
+    __shared__ uint32_t s_drop, s_drop2;
     if (threadIdx.x == 0) {
       s_m = 0;
       s_drop = 0;
+      s_drop2 = 0;
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -272,9 +276,10 @@ __global__ void __launch_bounds__(NT) k_sample_plan(SegPlan* __restrict__ plans,
         rk += (x > mc) || (x == mc && c2 < c);
       }
       if (rk >= m_wc) atomicAdd(&s_drop, mc);
+      if (rk >= m_wc2) atomicAdd(&s_drop2, mc);
     }
     __syncthreads();
-    const uint32_t keep_n = 20u * s_drop <= nsub ? m_wc : m_all;
+    const uint32_t keep_n = 20u * s_drop <= nsub ? m_wc : (20u * s_drop2 <= nsub ? max(m_wc, m_wc2) : m_all);
     for (uint32_t base = 0; base < nc; base += NT) {
       const uint32_t c = base + threadIdx.x;
       bool keep = false;

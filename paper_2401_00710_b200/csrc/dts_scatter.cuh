@@ -95,6 +95,16 @@ __device__ __forceinline__ void st_global(unsigned long long* p, unsigned long l
 __device__ __forceinline__ void st_global(unsigned long* p, unsigned long v) {
   asm volatile("st.global.u64 [%0], %1;" ::"l"(p), "l"(v));
 }
+// two adjacent elements (8- or 16-byte aligned) in one store
+__device__ __forceinline__ void st_global2(uint32_t* p, uint32_t a, uint32_t b) {
+  asm volatile("st.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(a), "r"(b));
+}
+__device__ __forceinline__ void st_global2(unsigned long long* p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b));
+}
+__device__ __forceinline__ void st_global2(unsigned long* p, unsigned long a, unsigned long b) {
+  asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b));
+}
 template <typename T>
 __device__ __forceinline__ T* opaque_ptr(T* p) {
   asm volatile("mov.b64 %0, %0;" : "+l"(p));

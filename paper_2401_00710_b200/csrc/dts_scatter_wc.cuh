@@ -36,16 +36,22 @@ template <> struct StPair<unsigned long long> {
   __device__ static T make(unsigned long long k, unsigned long long v) { return make_ulonglong2(k, v); }
 };
 
-template <typename K, int VB> struct WcTile {
+// WIDE = 1: the variant for heavy-key-rich waves (2^9 zones + up to 43
+// heavy keys + overflow = 600 bucket columns): the carries and per-warp
+// counters grow by 80 columns, paid for with smaller tiles where the two
+// tile buffers would not fit beside them (u32/u32: 12 records per thread,
+// 8-byte pairs: 6)
+template <typename K, int VB, int WIDE = 0> struct WcTile {
   // 512 threads: 768 (16.4 ms) and 1024 measured slower on C2 — the
   // per-bucket phases lengthen with the warp count
   static constexpr int NT = 512;
   static constexpr int NW = NT / 32;
   static constexpr int PT = 1;  // threads per bucket pair in the pair phases
-  static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? 14 : 7;
+  static constexpr bool PAIR8 = sizeof(K) == 8 && VB == 8;
+  static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? (WIDE && VB ? 12 : 14) : (WIDE && PAIR8 ? 6 : 7);
   static constexpr int WS = 32 * IPT;
   static constexpr int T = NT * IPT;
-  static constexpr int NBW = 520;  // bucket capacity (2^9 light + overflow + slack)
+  static constexpr int NBW = WIDE ? 600 : 520;  // bucket capacity (2^9 light + 2 per heavy key + overflow)
   static constexpr int C = (sizeof(K) == 8 || VB == 8) ? 8 : 16;  // chunk records (64 B)
   static constexpr int CP = C;  // carry stride (unpadded: the two half-warp runs of a carry step conflict at most 2-way)
   static constexpr int MAXCH = (T + (C - 1) * NBW) / C + 2;       // chunks per tile bound
@@ -53,8 +59,8 @@ template <typename K, int VB> struct WcTile {
   static constexpr int HZC = 520;
 };
 
-template <typename K, int VB> struct WcSmem {
-  using TL = WcTile<K, VB>;
+template <typename K, int VB, int WIDE = 0> struct WcSmem {
+  using TL = WcTile<K, VB, WIDE>;
   static constexpr size_t kb = a16((size_t)(TL::T + 8) * sizeof(K));
   static constexpr size_t vb = a16((size_t)(TL::T + 8) * VB);
   static constexpr size_t buf = 0;                                   // 2 x (keys | vals)
@@ -95,16 +101,16 @@ template <typename K, int VB> struct WcSmem {
 //   * each bucket's unfinished chunk moves to its carry slots.
 // At the end of a stripe the carries are flushed.
 // ---------------------------------------------------------------------------
-template <typename K, int VB>
-__global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
+template <typename K, int VB, int WIDE>
+__global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
     k_scatter_wc(const SegPlan* __restrict__ plans, const Blk* __restrict__ blks, uint32_t nblk,
                  uint32_t* __restrict__ ctr, const K* __restrict__ kin,
                  const typename ValOf<VB>::T* __restrict__ vin, K* __restrict__ kout,
                  typename ValOf<VB>::T* __restrict__ vout, const uint64_t* __restrict__ scan,
                  const K* __restrict__ heavy_pool, const uint32_t* __restrict__ hz_pool) {
   using V = typename ValOf<VB>::T;
-  using TL = WcTile<K, VB>;
-  using SL = WcSmem<K, VB>;
+  using TL = WcTile<K, VB, WIDE>;
+  using SL = WcSmem<K, VB, WIDE>;
   constexpr int NT = TL::NT, NW = TL::NW, IPT = TL::IPT, WS = TL::WS, T = TL::T, C = TL::C,
                 CP = TL::CP;
   constexpr uint32_t HW = TL::NBW / 2;
@@ -191,7 +197,7 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
     const uint32_t nb = P.nb, npair = (nb + 1) >> 1;
     if (B.seg != s_seg && (P.flags & PF_HEAVY)) {
       // zone table and heavy keys of the segment (sampler.py:76-100)
-      for (uint32_t i = tid; i <= P.nb && i < TL::HZC; i += NT) hz[i] = hz_pool[P.hz_base + i];
+      pack_zone_table(hz_pool + P.hz_base, 1u << P.gamma, hz);
       for (uint32_t i = tid; i < P.nheavy && i < (uint32_t)TL::HKC; i += NT) hk[i] = heavy_pool[P.heavy_base + i];
     }
     // per bucket: block offset -> chunk base, hole = fill (carry state kept
@@ -262,11 +268,13 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       // ---- route + per-warp rank; records into registers ----
       K key[IPT];
       V val[IPT];
-      uint32_t bk[IPT];  // bucket << 16 | rank within the warp's bucket run
+      // 2 * bucket << 16 | rank within the warp's bucket run (the high half is
+      // the byte offset of the bucket's u16 counter in the warp's row)
+      uint32_t bk[IPT];
       auto rank_one = [&](int i, uint32_t b) {
         const uint32_t sh = (b & 1u) << 4;
         const uint32_t old = atomicAdd(&mywh[b >> 1], 1u << sh);
-        bk[i] = (b << 16) | ((old >> sh) & 0xffffu);
+        bk[i] = (b << 17) | ((old >> sh) & 0xffffu);
       };
       if (full && !(P.flags & PF_HEAVY)) {
         const uint32_t shift = P.shift, mask = (1u << P.gamma) - 1u;
@@ -409,8 +417,11 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
 #pragma unroll
       for (int i = 0; i < IPT; ++i) {
         if (full || bk[i] != 0xFFFFFFFFu) {
-          const uint32_t b = bk[i] >> 16;
-          const uint32_t p = ((mywh[b >> 1] >> ((b & 1u) << 4)) & 0xffffu) + (bk[i] & 0xffffu);
+          // (the packed pair words read as a u16 array: bucket b's prefix is
+          // element b — one LDS.U16 at the byte offset kept in bk)
+          const uint32_t p = (uint32_t)*reinterpret_cast<const uint16_t*>(
+                                 reinterpret_cast<const unsigned char*>(mywh) + (bk[i] >> 16)) +
+                             (bk[i] & 0xffffu);
           st_put(p, key[i], VB ? val[i] : V(0));
           pk[p] = (uint16_t)(warp * WS + i * 32 + lane);
         }
@@ -426,6 +437,32 @@ __global__ void __launch_bounds__(WcTile<K, VB>::NT, 1)
       auto write_chunks = [&]() {
         const uint32_t nslot = nch * C;
         const uint32_t stoff = (uint32_t)(SL::buf + (size_t)cur * (SL::kb + SL::vb));  // staging pairs
+        if constexpr (AOS) {
+          // two adjacent slots of one chunk per thread: one descriptor load,
+          // one 8/16-byte store per column (chunks are 64-byte aligned, r is
+          // even); a pair cut by the hole stores its second slot alone
+          for (uint32_t q = 2 * tid; q < nslot; q += 2 * NT) {
+            const uint2 D = cdesc[q / C];
+            const uint32_t r = q % C;
+            const uint32_t hole = (D.y >> 18) & 15u, cc = (D.y >> 14) & 15u;
+            if (r + 1 < hole) continue;  // both slots: the previous stripe's records
+            const uint32_t cbase = (uint32_t)SL::ck + (D.y >> 22) * CP * (uint32_t)sizeof(PairT);
+            const uint32_t sbase = stoff + ((D.y & 0x3FFFu) - 16u) * (uint32_t)sizeof(PairT);
+            const uint32_t off0 = (r < cc ? cbase : sbase) + r * (uint32_t)sizeof(PairT);
+            const uint32_t off1 = (r + 1 < cc ? cbase : sbase) + (r + 1) * (uint32_t)sizeof(PairT);
+            const PairT p0 = *reinterpret_cast<const PairT*>(smem_raw + off0);
+            const PairT p1 = *reinterpret_cast<const PairT*>(smem_raw + off1);
+            const uint32_t d = D.x + r;
+            if (r >= hole) {
+              st_global2(ko_seg + d, (K)p0.x, (K)p1.x);
+              st_global2(vo_seg + d, (V)p0.y, (V)p1.y);
+            } else {
+              st_global(ko_seg + d + 1, (K)p1.x);
+              st_global(vo_seg + d + 1, (V)p1.y);
+            }
+          }
+          return;
+        }
         for (uint32_t q = tid; q < nslot; q += NT) {
           const uint2 D = cdesc[q / C];
           const uint32_t r = q % C;
