@@ -438,27 +438,42 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
         const uint32_t nslot = nch * C;
         const uint32_t stoff = (uint32_t)(SL::buf + (size_t)cur * (SL::kb + SL::vb));  // staging pairs
         if constexpr (AOS) {
-          // two adjacent slots of one chunk per thread: one descriptor load,
-          // one 8/16-byte store per column (chunks are 64-byte aligned, r is
-          // even); a pair cut by the hole stores its second slot alone
-          for (uint32_t q = 2 * tid; q < nslot; q += 2 * NT) {
-            const uint2 D = cdesc[q / C];
-            const uint32_t r = q % C;
-            const uint32_t hole = (D.y >> 18) & 15u, cc = (D.y >> 14) & 15u;
-            if (r + 1 < hole) continue;  // both slots: the previous stripe's records
-            const uint32_t cbase = (uint32_t)SL::ck + (D.y >> 22) * CP * (uint32_t)sizeof(PairT);
-            const uint32_t sbase = stoff + ((D.y & 0x3FFFu) - 16u) * (uint32_t)sizeof(PairT);
-            const uint32_t off0 = (r < cc ? cbase : sbase) + r * (uint32_t)sizeof(PairT);
-            const uint32_t off1 = (r + 1 < cc ? cbase : sbase) + (r + 1) * (uint32_t)sizeof(PairT);
-            const PairT p0 = *reinterpret_cast<const PairT*>(smem_raw + off0);
-            const PairT p1 = *reinterpret_cast<const PairT*>(smem_raw + off1);
-            const uint32_t d = D.x + r;
-            if (r >= hole) {
-              st_global2(ko_seg + d, (K)p0.x, (K)p1.x);
-              st_global2(vo_seg + d, (V)p0.y, (V)p1.y);
-            } else {
-              st_global(ko_seg + d + 1, (K)p1.x);
-              st_global(vo_seg + d + 1, (V)p1.y);
+          // (the SM's load/store pipe is the kernel's bound — SMEM wavefronts
+          // plus the 32 B/clk store port, tools/mb_store.cu, tools/mb_mio.cu —
+          // so conflict-free reads beat the fewer instructions of two adjacent
+          // slots per thread, whose LDS.64 pairs are 4-way conflicted)
+          // one slot per lane, two independent slots (q, q + 32) per thread:
+          // a warp's LDS.64 covers 32 consecutive pairs (no bank conflicts),
+          // keys and values leave as two 128-byte rows each
+          for (uint32_t q0 = 64 * (tid >> 5) + (tid & 31); q0 < nslot; q0 += 2 * NT) {
+            uint2 D[2];
+            uint32_t off[2], d[2];
+            bool on[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const uint32_t q = q0 + 32 * u;
+              D[u] = cdesc[(q < nslot ? q : q0) / C];
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const uint32_t q = q0 + 32 * u;
+              const uint32_t r = q % C;
+              const uint32_t hole = (D[u].y >> 18) & 15u, cc = (D[u].y >> 14) & 15u;
+              on[u] = q < nslot && r >= hole;
+              const uint32_t cbase = (uint32_t)SL::ck + (D[u].y >> 22) * CP * (uint32_t)sizeof(PairT);
+              const uint32_t sbase = stoff + ((D[u].y & 0x3FFFu) - 16u) * (uint32_t)sizeof(PairT);
+              off[u] = (r < cc ? cbase : sbase) + r * (uint32_t)sizeof(PairT);
+              d[u] = D[u].x + r;
+            }
+            PairT pr[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) pr[u] = *reinterpret_cast<const PairT*>(smem_raw + off[u]);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              if (on[u]) {
+                st_global(ko_seg + d[u], (K)pr[u].x);
+                st_global(vo_seg + d[u], (V)pr[u].y);
+              }
             }
           }
           return;
