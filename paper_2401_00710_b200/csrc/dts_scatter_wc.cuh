@@ -48,7 +48,16 @@ template <typename K, int VB, int WIDE = 0> struct WcTile {
   static constexpr int NW = NT / 32;
   static constexpr int PT = 1;  // threads per bucket pair in the pair phases
   static constexpr bool PAIR8 = sizeof(K) == 8 && VB == 8;
-  static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? (WIDE && VB ? 12 : 14) : (WIDE && PAIR8 ? 6 : 7);
+#ifndef DTS_WC_IPT4
+#define DTS_WC_IPT4 18
+#endif
+#ifndef DTS_WC_IPT8
+#define DTS_WC_IPT8 10
+#endif
+  // records per thread: the tile is as large as the registers allow (the
+  // records wait in registers from their loads to the placement); SMEM holds
+  // one staging buffer, so the wide variant keeps the same tile
+  static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? DTS_WC_IPT4 : DTS_WC_IPT8;
   static constexpr int WS = 32 * IPT;
   static constexpr int T = NT * IPT;
   static constexpr int NBW = WIDE ? 600 : 520;  // bucket capacity (2^9 light + 2 per heavy key + overflow)
@@ -61,10 +70,10 @@ template <typename K, int VB, int WIDE = 0> struct WcTile {
 
 template <typename K, int VB, int WIDE = 0> struct WcSmem {
   using TL = WcTile<K, VB, WIDE>;
-  static constexpr size_t kb = a16((size_t)(TL::T + 8) * sizeof(K));
-  static constexpr size_t vb = a16((size_t)(TL::T + 8) * VB);
-  static constexpr size_t buf = 0;                                   // 2 x (keys | vals)
-  static constexpr size_t pk = a16(buf + 2 * (kb + vb));             // staging: tile position (u16)
+  static constexpr size_t kb = a16((size_t)TL::T * sizeof(K));
+  static constexpr size_t vb = a16((size_t)TL::T * VB);
+  static constexpr size_t buf = 0;                                   // staging (keys | vals)
+  static constexpr size_t pk = a16(buf + kb + vb);                   // staging: tile position (u16)
   static constexpr size_t be = a16(pk + (size_t)(TL::T + 2) * 2);    // staging: bucket-run end bits
   static constexpr size_t ck = a16(be + (size_t)(TL::T / 32 + 2) * 4);  // carry keys
   static constexpr size_t cv = a16(ck + (size_t)TL::NBW * TL::CP * sizeof(K));
@@ -77,8 +86,7 @@ template <typename K, int VB, int WIDE = 0> struct WcSmem {
   static constexpr size_t hk = a16(cst + (size_t)(TL::NBW + 1) * 8);
   static constexpr size_t hz = a16(hk + (size_t)TL::HKC * sizeof(K));
   static constexpr size_t plan = a16(hz + (size_t)TL::HZC * 4);
-  static constexpr size_t bar = a16(plan + sizeof(SegPlan));
-  static constexpr size_t total = a16(bar + 16);
+  static constexpr size_t total = a16(plan + sizeof(SegPlan));
 };
 
 // ---------------------------------------------------------------------------
@@ -132,14 +140,10 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
   K* hk = reinterpret_cast<K*>(smem_raw + SL::hk);
   uint32_t* hz = reinterpret_cast<uint32_t*>(smem_raw + SL::hz);
   SegPlan* splan = reinterpret_cast<SegPlan*>(smem_raw + SL::plan);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + SL::bar);
-  auto bufk = [&](int b) { return reinterpret_cast<K*>(smem_raw + SL::buf + (size_t)b * (SL::kb + SL::vb)); };
-  auto bufv = [&](int b) {
-    return reinterpret_cast<V*>(smem_raw + SL::buf + (size_t)b * (SL::kb + SL::vb) + SL::kb);
-  };
+  K* const xk = reinterpret_cast<K*>(smem_raw + SL::buf);            // staging keys (or AoS pairs)
+  V* const xv = reinterpret_cast<V*>(smem_raw + SL::buf + SL::kb);   // staging values
   __shared__ uint32_t s_blk, s_fix, s_seg;
   __shared__ uint32_t s_wt[NW];
-  __shared__ uint32_t s_off[2][2];  // per buffer: key / value element offset of the tile
   __shared__ Blk s_B;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t* mywh = wh + warp * HW;
@@ -149,33 +153,12 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
   using PairT = typename StPair<K>::T;
 
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_mbar_init();
     s_fix = 0u;
     s_seg = 0xFFFFFFFFu;
   }
   for (uint32_t i = tid; i < NW * HW; i += NT) wh[i] = 0u;
-  uint32_t ph0 = 0u, ph1 = 0u;
-  int cur = 0;
   [[maybe_unused]] constexpr bool ph_on = DTS_PHASE_PROF == 1;
   PH_INIT
-
-  // thread 0: stream records [g0, g0+tn) into buffer b
-  auto issue_tile = [&](uint64_t g0, uint32_t tn, int b) {
-    const char* ks;
-    uint32_t ko, vo = 0;
-    const uint32_t kbytes = tile_span<K>(kin, g0, tn, ks, ko);
-    const char* vs = nullptr;
-    uint32_t vbytes = 0;
-    if (VB) vbytes = tile_span<V>(vin, g0, tn, vs, vo);
-    s_off[b][0] = ko;
-    s_off[b][1] = vo;
-    fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&bar[b], kbytes + vbytes);
-    tma_load_1d(bufk(b), ks, kbytes, &bar[b]);
-    if (VB) tma_load_1d(bufv(b), vs, vbytes, &bar[b]);
-  };
 
   for (;;) {
     __syncthreads();
@@ -220,25 +203,58 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
       const uint64_t r = len - (uint64_t)kt * T;
       return (uint32_t)(r < (uint64_t)T ? r : (uint64_t)T);
     };
+    // ---- records of a tile: global -> registers by coalesced streaming
+    // loads (warp instruction i of warp w covers tile positions
+    // w*WS + i*32 + lane), issued one phase ahead — right after the previous
+    // tile's placement, so they land behind its write-out and carries; a
+    // TMA bulk prefetch pulls the tile into L2 one tile earlier.  The tile
+    // never passes through SMEM on its way in (the load/store pipe is the
+    // bound: no TMA write + LDS per record), and the one SMEM tile buffer is
+    // the staging area.
+    K key[IPT];
+    V val[IPT];
+    auto load_tile = [&](uint32_t kt) {
+      const uint32_t tn = tile_n(kt);
+      const K* gk = kin + B.begin + (uint64_t)kt * T + warp * WS + lane;
+      const V* gv = VB ? vin + B.begin + (uint64_t)kt * T + warp * WS + lane : nullptr;
+      if (tn == (uint32_t)T) {
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          key[i] = __ldcs(gk + i * 32);
+          if (VB) val[i] = __ldcs(gv + i * 32);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          if ((uint32_t)(warp * WS + i * 32 + lane) < tn) {
+            key[i] = __ldcs(gk + i * 32);
+            if (VB) val[i] = __ldcs(gv + i * 32);
+          }
+        }
+      }
+    };
+    auto prefetch_tile = [&](uint32_t kt) {  // (one thread)
+      const char* src;
+      uint32_t off;
+      const uint64_t g0 = B.begin + (uint64_t)kt * T;
+      const uint32_t kbytes = tile_span<K>(kin, g0, tile_n(kt), src, off);
+      prefetch_l2(src, kbytes);
+      if (VB) {
+        const uint32_t vbytes = tile_span<V>(vin, g0, tile_n(kt), src, off);
+        prefetch_l2(src, vbytes);
+      }
+    };
     PH(9)
-    if (tid == 0 && ntl) issue_tile(B.begin, tile_n(0), cur);
+    if (ntl) load_tile(0);
+    if (tid == 0 && ntl > 1) prefetch_tile(1);
     __syncthreads();
     if (tid == 0) s_seg = B.seg;
 
-    for (uint32_t kt = 0; kt < ntl; ++kt, cur ^= 1) {
+    for (uint32_t kt = 0; kt < ntl; ++kt) {
       PH(0)
       const uint32_t tn = tile_n(kt);
       const bool full = tn == (uint32_t)T;
-      if (cur == 0) {
-        mbar_wait(&bar[0], ph0);
-        ph0 ^= 1u;
-      } else {
-        mbar_wait(&bar[1], ph1);
-        ph1 ^= 1u;
-      }
-      PH(1)
-      K* xk = bufk(cur);
-      V* xv = bufv(cur);
+      if (tid == 0 && kt + 2 < ntl) prefetch_tile(kt + 2);
       // staging slot accessors (AoS pairs when key and value widths match;
       // the pair array spans this tile's key+value buffer)
       auto st_put = [&](uint32_t p, K k, V v) {
@@ -259,15 +275,11 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
           if (VB) v = xv[p];
         }
       };
-      const K* ik = xk + s_off[cur][0];
-      const V* iv = xv + s_off[cur][1];
 
       // (run-end bits of this tile: set in the pair phase below; the last
       // reads of the previous tile's were before its write-out barrier)
       for (uint32_t i = tid; i < (uint32_t)(T / 32 + 2); i += NT) bend[i] = 0u;
-      // ---- route + per-warp rank; records into registers ----
-      K key[IPT];
-      V val[IPT];
+      // ---- route + per-warp rank ----
       // 2 * bucket << 16 | rank within the warp's bucket run (the high half is
       // the byte offset of the bucket's u16 counter in the warp's row)
       uint32_t bk[IPT];
@@ -283,9 +295,6 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
         const uint32_t ovfb = ovf ? nb - 1 : ((uint32_t)(~K(0) >> shift) & mask);
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
-          const uint32_t e = warp * WS + i * 32 + lane;
-          key[i] = ik[e];
-          if (VB) val[i] = iv[e];
           rank_one(i, key[i] >= thr ? ovfb : ((uint32_t)(key[i] >> shift) & mask));
           __syncwarp();
         }
@@ -295,20 +304,12 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
         for (int i = 0; i < IPT; ++i) {
           const uint32_t e = warp * WS + i * 32 + lane;
           bk[i] = 0xFFFFFFFFu;
-          if (e < tn) {
-            key[i] = ik[e];
-            if (VB) val[i] = iv[e];
-            rank_one(i, R(key[i]));
-          }
+          if (e < tn) rank_one(i, R(key[i]));
           __syncwarp();
         }
       }
       __syncthreads();
       PH(2)
-      // the other buffer (previous tile's staging) is free: stream the next tile
-      if (tid == 0) {
-        if (kt + 1 < ntl) issue_tile(B.begin + (uint64_t)(kt + 1) * T, tile_n(kt + 1), cur ^ 1);
-      }
 
       // ---- bucket pair j = tid: prefix over warps; packed scan of
       // (tile count | complete chunks of carry + run) ----
@@ -430,13 +431,15 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
       for (uint32_t i = lane; i < HW; i += 32) mywh[i] = 0u;
       __syncthreads();
       PH(5)
+      // the records sit in the staging area: the next tile's loads start now
+      if (kt + 1 < ntl) load_tile(kt + 1);
 
       // ---- stable order check (within a bucket, tile positions ascend) and
       // write-out of every complete chunk: slot r of bucket b's current chunk
       // run (carry slots [0, cc) first, then the staging run) ----
       auto write_chunks = [&]() {
         const uint32_t nslot = nch * C;
-        const uint32_t stoff = (uint32_t)(SL::buf + (size_t)cur * (SL::kb + SL::vb));  // staging pairs
+        const uint32_t stoff = (uint32_t)SL::buf;  // staging pairs
         if constexpr (AOS) {
           // (the SM's load/store pipe is the kernel's bound — SMEM wavefronts
           // plus the 32 B/clk store port, tools/mb_store.cu, tools/mb_mio.cu —
