@@ -404,6 +404,12 @@ struct Sorter {
   uint32_t choose_gamma(uint64_t len, uint32_t remaining) const {
     const uint64_t target = std::max<uint64_t>(1, thr / 2);
     uint32_t need = ceil_log2_u64((len + target - 1) / target);
+    // (a segment just above the base case is usually rich in duplicates —
+    // near-unique keys would have fitted: a 2-bit digit per level leaves
+    // skewed inputs a tail of levels that are all launch latency, Zipf 1.0:
+    // levels 3-7 hold 5 % of the records; at least gamma_min bits at once)
+    static const uint32_t gamma_min = (uint32_t)env_int("DTS_GAMMA_MIN", 6);
+    need = std::max(need, gamma_min);
     uint32_t g = std::min(need, gcap);
     g = std::min(g, remaining);
     return std::max<uint32_t>(g, 1);
@@ -749,10 +755,11 @@ struct Sorter {
     uint64_t* dpart = (uint64_t*)meta.take(std::max<uint64_t>(1, nch) * 8);
     uint64_t* dbs = (uint64_t*)meta.take(bs_total * 8);
     uint8_t* dkinds = (uint8_t*)meta.take(bs_total);
+    uint16_t* dzones = (uint16_t*)meta.take(bs_total * 2);
     uint32_t* dtile_blk = (uint32_t*)meta.take(std::max<uint64_t>(1, ntile) * 4);
     uint32_t* dblk_tile0 = (uint32_t*)meta.take(std::max<size_t>(1, blk_tile0.size()) * 4);
     uint32_t* dstatus = (uint32_t*)meta.take(std::max<uint64_t>(1, ntile) * (nbc / 2) * 4);
-    if (!dblks || !dcnt || !dscan || !dpart || !dbs || !dkinds || !dtile_blk || !dblk_tile0 ||
+    if (!dblks || !dcnt || !dscan || !dpart || !dbs || !dkinds || !dzones || !dtile_blk || !dblk_tile0 ||
         !dstatus)
       return fail(DTS_ENOMEM, "workspace too small for level metadata");
 
@@ -808,7 +815,7 @@ struct Sorter {
     {
       Timer::Ev ev;
       tm.begin(DTS_K_BOUNDS, ev);
-      k_bucket_bounds<<<(unsigned)ns, 256, 0, st>>>(dplans, dscan, dhz, dbs, dkinds);
+      k_bucket_bounds<<<(unsigned)ns, 256, 0, st>>>(dplans, dscan, dhz, dbs, dkinds, dzones);
       tm.end(ev, bs_total);
       DTS_TRY(check_launch("k_bucket_bounds"));
     }
@@ -835,9 +842,10 @@ struct Sorter {
       CUDA_TRY(cudaEventRecord(ev_fork, st));
       CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
     }
+    static const uint32_t cls_rules = (uint32_t)env_int("DTS_CLS_RULES", 1);
     CUDA_TRY(cudaMemsetAsync(dcc, 0, 8 * sizeof(unsigned long long), cs));
     k_classify<<<(unsigned)ns, CLS_NT, 0, cs>>>(dplans, dbs, dkinds, (uint32_t)W, out_src, thr, COPY_CHUNK,
-                                             dspan, dcopy, dnext, dcc);
+                                             dspan, dcopy, dnext, dcc, dzones, cls_rules);
     tm.launches += 1;
     DTS_TRY(check_launch("k_classify"));
     DTS_TRY(g_pin_back.ensure(256 + align256(pb) + 256));
@@ -936,7 +944,7 @@ struct Sorter {
     else
       nbmax = 1u << g;
     const uint64_t tiles = s.len / 2560 + rows + 1;
-    return 88 + rows * 28 + nbmax * rows * 12 + (nbmax + 1) * 9 + (1u << g) * 12 + 4096 +
+    return 88 + rows * 28 + nbmax * rows * 12 + (nbmax + 1) * 11 + (1u << g) * 12 + 4096 +
            tiles * (4 + ((nbmax + 1) & ~1ull) * 4);
   }
 
@@ -1143,7 +1151,7 @@ int partition_impl(const void* keys, const void* vals, uint64_t n, uint64_t gbas
     DTS_TRY(check_launch("k_histogram(split)"));
   }
   DTS_TRY(flat_scan(dcnt, cnt_total, dscan, dpart, tm));
-  k_bucket_bounds<<<1, 256, 0, st>>>(dplan, dscan, nullptr, dbs, dkinds);
+  k_bucket_bounds<<<1, 256, 0, st>>>(dplan, dscan, nullptr, dbs, dkinds, nullptr);
   DTS_TRY(check_launch("k_bucket_bounds(split)"));
   {
     using TL = ScatterTile<K, VB>;

@@ -63,6 +63,7 @@ struct Span {
   uint32_t src;
 };
 constexpr uint32_t SPAN_NOBOUND = 255u;
+constexpr uint32_t LOCAL_NB = 12u;  // the base case's one-pass counting takes spans differing in <= LOCAL_NB bits
 
 // A finished range that must be copied T -> A (dtsort.py:111-124).
 struct CopyR {

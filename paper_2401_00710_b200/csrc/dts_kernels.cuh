@@ -458,11 +458,13 @@ __global__ void __launch_bounds__(256) k_bucket_bounds(const SegPlan* __restrict
                                                        const uint64_t* __restrict__ scan,
                                                        const uint32_t* __restrict__ hz_pool,
                                                        uint64_t* __restrict__ bstart,
-                                                       uint8_t* __restrict__ kinds) {
+                                                       uint8_t* __restrict__ kinds,
+                                                       uint16_t* __restrict__ zones) {
   const SegPlan P = plans[blockIdx.x];
   for (uint32_t b = threadIdx.x; b <= P.nbmax; b += blockDim.x) {
     uint64_t v = P.len;
     uint8_t kind = KIND_PAD;
+    uint32_t zone = b;  // the bucket's digit value (k_classify: key bound of merged spans)
     if (b < P.nb) {
       v = scan[P.cnt_base + (uint64_t)b * P.nrows] - P.scanbase;
       if ((P.flags & PF_OVF) && b == P.nb - 1) {
@@ -477,12 +479,14 @@ __global__ void __launch_bounds__(256) k_bucket_bounds(const SegPlan* __restrict
         }
         const uint32_t off = b - (lo + 2u * hz[lo]);
         kind = (off & 1u) ? KIND_HEAVY : KIND_LIGHT;
+        zone = lo;
       } else {
         kind = KIND_LIGHT;
       }
     }
     bstart[P.bs_base + b] = v;
     kinds[P.bs_base + b] = kind;
+    if (zones) zones[P.bs_base + b] = (uint16_t)zone;
   }
 }
 
@@ -557,7 +561,8 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(const SegPlan* __restrict__
                                                      uint32_t out_src, uint64_t thr, uint32_t copy_chunk,
                                                      Span* __restrict__ spans, CopyR* __restrict__ copies,
                                                      NextSeg* __restrict__ next,
-                                                     unsigned long long* __restrict__ ctr) {
+                                                     unsigned long long* __restrict__ ctr,
+                                                     const uint16_t* __restrict__ zones, uint32_t rules) {
   enum : uint32_t { T_EMPTY = 0, T_CAND = 1, T_FLUSH = 2, T_COPY = 3, T_NEXT = 4 };
   __shared__ uint64_t s_bs[CLS_MAXB];
   __shared__ uint32_t s_ty[CLS_MAXB];
@@ -623,8 +628,16 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(const SegPlan* __restrict__
     }
     if (rec) atomicAdd(&s_acc[3], rec);
   } else if (threadIdx.x == 0) {
-    uint32_t nsp = 0;
-    bool have = false;
+    // Merge rules (`rules` bits, DTS_CLS_RULES): (1) a bucket of equal keys
+    // (heavy run, exhausted bucket) stays alone — the base case only copies
+    // it, while merged into a neighbour it is a huge equal-key group of a
+    // wide span (C4 exp 1e-5: local sort 2.3 -> 1.7 ms).  (2) light buckets
+    // that fit the base case's one-pass counting (<= LOCAL_NB differing
+    // bits) merge only while the span still does — measured slower (Zipf 1.2
+    // local sort 2.8 -> 5.3 ms: the extra small spans cost more than the LSD
+    // passes they avoid), off by default.
+    uint32_t nsp = 0, first_z = 0;
+    bool have = false, cur_equal = false;
     Span cur{0, 0, 0};
     unsigned long long spanrec = 0;
     for (uint32_t b = 0; b < nb; ++b) {
@@ -634,16 +647,31 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(const SegPlan* __restrict__
         const uint64_t lo = P.offset + s_bs[b];
         const uint32_t sz = (uint32_t)(s_bs[b + 1] - s_bs[b]);
         spanrec += sz;
-        const uint32_t bound = kinds[P.bs_base + b] == KIND_LIGHT ? P.shift : SPAN_NOBOUND;
-        if (have && cur.offset + cur.len == lo && cur.len + sz <= thr) {
-          cur.len += sz;  // several buckets: the keys agree above the digit
+        const uint8_t kind = kinds[P.bs_base + b];
+        const bool equal = (rules & 1u) && (kind == KIND_HEAVY || (kind == KIND_LIGHT && P.shift == 0));
+        const uint32_t bound = kind == KIND_LIGHT ? P.shift : SPAN_NOBOUND;
+        bool merge = have && !equal && !cur_equal && cur.offset + cur.len == lo && cur.len + sz <= thr;
+        uint32_t nbd = SPAN_NOBOUND;
+        if (merge) {
           const uint32_t cb = (cur.src >> 8) & 255u;
-          const uint32_t nbd = (cb == SPAN_NOBOUND || bound == SPAN_NOBOUND) ? SPAN_NOBOUND : P.shift + P.gamma;
+          if (cb != SPAN_NOBOUND && bound != SPAN_NOBOUND) {
+            // several light buckets: the keys agree above the highest bit in
+            // which their digits differ (sub-buckets of one zone, split at
+            // its heavy keys: above the digit)
+            const uint32_t z = zones[P.bs_base + b];
+            nbd = P.shift + (32u - (uint32_t)__clz((int)(first_z ^ z)));
+            if ((rules & 2u) && P.shift <= LOCAL_NB && nbd > LOCAL_NB) merge = false;
+          }
+        }
+        if (merge) {
+          cur.len += sz;
           cur.src = (cur.src & 255u) | (nbd << 8);
         } else {
           if (have) s_sp[nsp++] = cur;
           cur = Span{lo, sz, out_src | (bound << 8)};
           have = true;
+          cur_equal = equal;
+          first_z = zones[P.bs_base + b];
         }
       } else {
         if (have) s_sp[nsp++] = cur;

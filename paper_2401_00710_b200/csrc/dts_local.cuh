@@ -30,6 +30,7 @@ template <typename K, int VB> struct LocalTile {
   static constexpr int NB = 12;        // nibble counting path: spans differing in <= NB bits
   static constexpr int CB = 13;        // packed counting path: top CB differing bits
   static constexpr int FIXMAX = 64;    // packed counting path: largest equal-key group
+  static_assert(NB == (int)LOCAL_NB, "k_classify's merge rule follows the counting path's width");
 };
 
 // Compile-time SMEM layout: two span buffers (TMA double buffering), the
