@@ -662,7 +662,11 @@ struct Sorter {
     nbc = (nbc + 1) & ~1u;
     // (the wide variant takes heavy-key-rich waves of up to 600 columns)
     const bool wc = wc_env != 0 && nbc <= (wide_env ? (uint32_t)WcTile<K, VB, 1>::NBW : (uint32_t)WcTile<K, VB>::NBW);
-    const bool wide = wc && nbc > (uint32_t)WcTile<K, VB>::NBW;
+    // (and every wave with heavy keys: the variant writes the many chunk
+    // descriptors of a heavy bucket cooperatively)
+    bool any_heavy = false;
+    for (size_t i = 0; i < ns && !any_heavy; ++i) any_heavy = (plans[i].flags & PF_HEAVY) != 0;
+    const bool wide = wc && wide_env && (nbc > (uint32_t)WcTile<K, VB>::NBW || any_heavy);
     const uint64_t WT = wide ? (uint64_t)WcTile<K, VB, 1>::T : (uint64_t)WcTile<K, VB>::T;
     static const int wc_lbs_env = env_int("DTS_WC_LBS", 0);
     const uint64_t wc_lbs = wc_lbs_env > 0 ? (uint64_t)wc_lbs_env : WC_LBS;

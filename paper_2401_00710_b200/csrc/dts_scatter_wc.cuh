@@ -145,6 +145,15 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
   __shared__ uint32_t s_blk, s_fix, s_seg;
   __shared__ uint32_t s_wt[NW];
   __shared__ Blk s_B;
+  // WIDE (waves with heavy keys): a bucket with many complete chunks in a
+  // tile — a heavy key's — has its descriptors written by the whole CTA (one
+  // thread per chunk) after the pair phase, not by the pair's owner in a
+  // serial loop (Zipf 1.5: scatter 11.1 -> 10.3 ms).  Not in the plain
+  // variant: the extra code cost C2 2 %.
+  constexpr bool COOP = WIDE != 0;
+  constexpr uint32_t COOP_MIN = 16, COOP_CAP = COOP ? T / ((COOP_MIN - 1) * C) + 2 : 1;  // (> COOP_MIN chunks hold > (COOP_MIN - 1) * C records)
+  __shared__ uint32_t s_nlong;
+  __shared__ uint32_t s_long[COOP_CAP][5];  // {first chunk, chunks, dest, staging index | bucket, first-chunk bits}
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t* mywh = wh + warp * HW;
   // key and value of the same width: staging slots and carry slots are
@@ -155,6 +164,7 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
   if (tid == 0) {
     s_fix = 0u;
     s_seg = 0xFFFFFFFFu;
+    s_nlong = 0u;
   }
   for (uint32_t i = tid; i < NW * HW; i += NT) wh[i] = 0u;
   [[maybe_unused]] constexpr bool ph_on = DTS_PHASE_PROF == 1;
@@ -386,6 +396,15 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
           // descriptors of this pair's complete chunks
           auto chunks = [&](uint32_t b, uint2 I, uint32_t f, uint32_t t, uint32_t g0) {
             const uint32_t cc = I.x & 0xffffu, ch = I.x >> 16;
+            if (COOP && f > COOP_MIN) {
+              const uint32_t at = atomicAdd(&s_nlong, 1u);
+              s_long[at][0] = g0;
+              s_long[at][1] = f;
+              s_long[at][2] = I.y;
+              s_long[at][3] = (t - cc + 16u) | (b << 22);
+              s_long[at][4] = (cc << 14) | (ch << 18);
+              return;
+            }
             for (uint32_t k = 0; k < f; ++k)
               cdesc[g0 + k] = make_uint2(I.y + k * C, (t - cc + k * C + 16u) | (k ? 0u : ((cc << 14) | (ch << 18))) | (b << 22));
           };
@@ -413,6 +432,15 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
       }
       __syncthreads();
       PH(4)
+      if constexpr (COOP) {
+        const uint32_t nl = s_nlong;
+        for (uint32_t e = 0; e < nl; ++e) {
+          const uint32_t g0 = s_long[e][0], f = s_long[e][1], dst = s_long[e][2], sb = s_long[e][3],
+                         fb = s_long[e][4];
+          for (uint32_t k = tid; k < f; k += NT)
+            cdesc[g0 + k] = make_uint2(dst + k * C, (sb + k * C) | (k ? 0u : fb));
+        }
+      }
 
       // ---- placement into the staging area (this tile's buffer) ----
 #pragma unroll
@@ -431,6 +459,7 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
       for (uint32_t i = lane; i < HW; i += 32) mywh[i] = 0u;
       __syncthreads();
       PH(5)
+      if (COOP && tid == 0) s_nlong = 0u;
       // the records sit in the staging area: the next tile's loads start now
       if (kt + 1 < ntl) load_tile(kt + 1);
 
