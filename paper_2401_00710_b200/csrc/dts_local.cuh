@@ -118,7 +118,9 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
 
   const uint32_t G = gridDim.x;
   const uint32_t nspan = *nspan_p;  // device-resident count (k_classify)
-  Span nextS;  // thread 0: descriptor of the span after the one in flight
+  // (one thread's) descriptor of the span after the one in flight: in SMEM —
+  // a register copy costs every thread 4 registers of a kernel at its cap
+  __shared__ Span s_next;
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -130,7 +132,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
   __syncthreads();
   if (tid == NT - 1) {
     if (blockIdx.x < nspan) issue(spans[blockIdx.x], 0);
-    if (blockIdx.x + G < nspan) nextS = spans[blockIdx.x + G];
+    if (blockIdx.x + G < nspan) s_next = spans[blockIdx.x + G];
   }
   for (uint32_t i = tid; i < (uint32_t)(SL::cnt_bytes / 4); i += NT) cnt[i] = 0u;
   __syncthreads();
@@ -181,8 +183,8 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
     // stream the next span into the other buffer (freed by the previous
     // iteration's final barrier); fetch the descriptor after it
     if (tid == NT - 1) {
-      if (sidx + G < nspan) issue(nextS, cur ^ 1);
-      if (sidx + 2 * G < nspan) nextS = spans[sidx + 2 * G];
+      if (sidx + G < nspan) issue(s_next, cur ^ 1);
+      if (sidx + 2 * G < nspan) s_next = spans[sidx + 2 * G];
     }
     if (!known) {
       diff = 0;
