@@ -14,5 +14,5 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_
   -o gpurun_out/r2c_full python tools/prof_sort.py 1e9 > gpurun_out/r2c_full.log 2>&1
 # the heavy-key variants on a skewed input: histogram + WC scatter (wide) of Zipf 1.5's first level
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_histogram|k_scatter_wc" -c 2 \
-  -o gpurun_out/r2c_zipf15 python tools/prof_cfg.py c3-zipf1.5 > gpurun_out/r2c_zipf15.log 2>&1
+  -o gpurun_out/r2c_zipf15 python tools/prof_cfg.py c3-zipf1.5 1e9 0 > gpurun_out/r2c_zipf15.log 2>&1
 ls -la gpurun_out $P
