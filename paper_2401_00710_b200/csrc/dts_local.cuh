@@ -23,7 +23,16 @@ template <typename K, int VB> struct LocalTile {
   // stable counting path below); 2 CTAs per SM
   static constexpr int NT = 256;
   static constexpr int NW = NT / 32;
-  static constexpr int IPT = (sizeof(K) == 4 && VB <= 4) ? 18 : 10;
+#ifndef DTS_LOCAL_IPT8
+#define DTS_LOCAL_IPT8 18
+#endif
+  // 8-byte columns: ONE span buffer (the next span streams in once this one
+  // has left; the SM's other CTA covers the wait), so a span holds as many
+  // records as with 4-byte columns — with two buffers the capacity was 2560
+  // records and every 64-bit config of BASELINE.json needed a third
+  // distribution pass for buckets of ~3800 records
+  static constexpr bool SINGLE = !(sizeof(K) == 4 && VB <= 4);
+  static constexpr int IPT = SINGLE ? DTS_LOCAL_IPT8 : 18;
   static constexpr int WS = 32 * IPT;  // records per warp sub-tile
   static constexpr int CAP = NT * IPT; // records per span
   static constexpr int RB = 8;         // LSD radix bits per pass (fallback path)
@@ -42,8 +51,8 @@ template <typename K, int VB> struct LocalSmem {
   static constexpr size_t vcap = (size_t)(TL::CAP + 8) * VB;
   static constexpr size_t k0 = 0;
   static constexpr size_t v0 = a16(k0 + kcap);
-  static constexpr size_t k1 = a16(v0 + vcap);
-  static constexpr size_t v1 = a16(k1 + kcap);
+  static constexpr size_t k1 = TL::SINGLE ? k0 : a16(v0 + vcap);
+  static constexpr size_t v1 = TL::SINGLE ? v0 : a16(k1 + kcap);
   static constexpr size_t si = a16(v1 + vcap);
   static constexpr size_t cnt = a16(si + (size_t)TL::CAP * 4);
   static constexpr size_t cnt_bytes = ((size_t)1 << TL::CB) * 2;
@@ -142,6 +151,12 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
   PH_INIT
   for (uint32_t sidx = blockIdx.x; sidx < nspan; sidx += G, cur ^= 1) {
     PH(9)
+    if (TL::SINGLE && sidx != blockIdx.x && tid == NT - 1) {
+      // one buffer: every thread is past the previous span's last read (its
+      // final barrier), the span's descriptor was fetched an iteration ago
+      issue(s_next, cur);
+      if (sidx + G < nspan) s_next = spans[sidx + G];
+    }
     if (cur == 0) {
       mbar_wait(&bar[0], ph0);
       ph0 ^= 1u;
@@ -182,7 +197,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
     PH(1)
     // stream the next span into the other buffer (freed by the previous
     // iteration's final barrier); fetch the descriptor after it
-    if (tid == NT - 1) {
+    if (!TL::SINGLE && tid == NT - 1) {
       if (sidx + G < nspan) issue(s_next, cur ^ 1);
       if (sidx + 2 * G < nspan) s_next = spans[sidx + 2 * G];
     }
