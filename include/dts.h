@@ -87,7 +87,9 @@ typedef struct dts_report {
 
 /* Device workspace needed by dts_sort / dts_partition for n records of the
  * given widths (key_bytes 4|8, val_bytes 0|4|8).  Holds the temporary
- * buffer twin (dtsort.py:92-99 `np.empty_like`) plus per-level metadata. */
+ * buffer twin (dtsort.py:92-99 `np.empty_like`), 2 bytes per record of bucket
+ * ids (heavy-key segments: the histogram's routing result, reused by the
+ * scatter) and per-level metadata. */
 size_t dts_workspace_bytes(uint64_t n, int key_bytes, int val_bytes);
 
 /* Stable ascending sort in place — replaces dt_sort / plain_msd_sort / _run

@@ -371,6 +371,7 @@ struct Sorter {
   V* Av;
   K* Tk;
   V* Tv;
+  uint16_t* bid = nullptr;  // bucket ids of heavy segments' records (k_histogram -> k_scatter_wc)
   uint64_t n;
   Bump meta;
   dts_config cfg;
@@ -806,12 +807,12 @@ struct Sorter {
       CUDA_TRY(cudaMemsetAsync(dctr, 0, 16, st));
       Timer::Ev ev;
       tm.begin(DTS_K_HIST, ev);
-      auto fn = k_histogram<K, HIST_NT, false>;
+      auto fn = wide ? k_histogram<K, HIST_NT, false, true> : k_histogram<K, HIST_NT, false, false>;
       const size_t sm = hist_layout(sizeof(K), caps, false).total;
       DTS_TRY(set_smem(fn, sm));
       const int grid = persistent_grid(fn, HIST_NT, sm, (uint32_t)blks.size());
       fn<<<grid, HIST_NT, sm, st>>>(dplans, dblks, (uint32_t)blks.size(), dctr, ink, dcnt, dheavy,
-                                    dhz, nullptr, 0, caps);
+                                    dhz, nullptr, 0, caps, wide ? bid : nullptr);
       tm.end(ev, wave_recs);
       DTS_TRY(check_launch("k_histogram"));
     }
@@ -868,7 +869,7 @@ struct Sorter {
       DTS_TRY(set_smem(fn, sm));
       const int grid = persistent_grid(fn, WcTile<K, VB>::NT, sm, (uint32_t)blks.size());
       fn<<<grid, WcTile<K, VB>::NT, sm, st>>>(dplans, dblks, (uint32_t)blks.size(), dctr + 1, ink, inv,
-                                              outk, outv, dscan, dheavy, dhz);
+                                              outk, outv, dscan, dheavy, dhz, wide ? bid : nullptr);
       tm.end(ev, wave_recs);
       DTS_TRY(check_launch("k_scatter_wc"));
     } else {
@@ -1006,8 +1007,10 @@ int sort_impl(void* keys, void* vals, uint64_t n, void* ws, size_t wsb, const dt
   const size_t kbytes = align256(n * sizeof(K)), vbytes = align256(n * (size_t)VB);
   S.Tk = (K*)w;
   S.Tv = VB ? (V*)(w + kbytes) : nullptr;
-  S.meta.base = w + kbytes + vbytes;
-  S.meta.cap = wsb - kbytes - vbytes;
+  const size_t bbytes = align256(n * 2);
+  S.bid = (uint16_t*)(w + kbytes + vbytes);
+  S.meta.base = w + kbytes + vbytes + bbytes;
+  S.meta.cap = wsb - kbytes - vbytes - bbytes;
   S.n = n;
   S.cfg = *cfg;
   S.rep = rep;
@@ -1151,7 +1154,7 @@ int partition_impl(const void* keys, const void* vals, uint64_t n, uint64_t gbas
     DTS_TRY(set_smem(fn, sm));
     const int grid = persistent_grid(fn, HIST_NT, sm, (uint32_t)blks.size());
     fn<<<grid, HIST_NT, sm, st>>>(dplan, dblks, (uint32_t)blks.size(), dctr, (const K*)keys, dcnt,
-                                  dsk, nullptr, dsi, gbase, caps);
+                                  dsk, nullptr, dsi, gbase, caps, nullptr);
     DTS_TRY(check_launch("k_histogram(split)"));
   }
   DTS_TRY(flat_scan(dcnt, cnt_total, dscan, dpart, tm));
@@ -1360,7 +1363,8 @@ int dts_debug_phases(unsigned long long* out, int n, int reset) {
 
 size_t dts_workspace_bytes(uint64_t n, int key_bytes, int val_bytes) {
   if (!valid_widths(key_bytes, val_bytes)) return 0;
-  return align256(n * (size_t)key_bytes) + align256(n * (size_t)val_bytes) + meta_bytes(n);
+  // twin T (keys, values), 2 bytes per record of bucket ids, metadata
+  return align256(n * (size_t)key_bytes) + align256(n * (size_t)val_bytes) + align256(n * 2) + meta_bytes(n);
 }
 
 int dts_sort(void* keys, void* vals, uint64_t n, int kb, int vb, void* ws, size_t wsb,

@@ -115,7 +115,8 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
                  uint32_t* __restrict__ ctr, const K* __restrict__ kin,
                  const typename ValOf<VB>::T* __restrict__ vin, K* __restrict__ kout,
                  typename ValOf<VB>::T* __restrict__ vout, const uint64_t* __restrict__ scan,
-                 const K* __restrict__ heavy_pool, const uint32_t* __restrict__ hz_pool) {
+                 const K* __restrict__ heavy_pool, const uint32_t* __restrict__ hz_pool,
+                 const uint16_t* __restrict__ bid) {
   using V = typename ValOf<VB>::T;
   using TL = WcTile<K, VB, WIDE>;
   using SL = WcSmem<K, VB, WIDE>;
@@ -223,6 +224,11 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
     // the staging area.
     K key[IPT];
     V val[IPT];
+    // WIDE (waves with heavy keys): the bucket ids k_histogram kept for a
+    // heavy segment come in with the records — no routing in the rank phase
+    // (the router's two dependent SMEM loads per record made it 4x C2's)
+    [[maybe_unused]] uint32_t pb[WIDE ? IPT : 1];
+    const bool use_bid = WIDE != 0 && bid != nullptr && (P.flags & PF_HEAVY) != 0;
     auto load_tile = [&](uint32_t kt) {
       const uint32_t tn = tile_n(kt);
       const K* gk = kin + B.begin + (uint64_t)kt * T + warp * WS + lane;
@@ -240,6 +246,14 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
             key[i] = __ldcs(gk + i * 32);
             if (VB) val[i] = __ldcs(gv + i * 32);
           }
+        }
+      }
+      if constexpr (WIDE != 0) {
+        if (use_bid) {
+          const uint16_t* gb = bid + B.begin + (uint64_t)kt * T + warp * WS + lane;
+#pragma unroll
+          for (int i = 0; i < IPT; ++i)
+            if ((uint32_t)(warp * WS + i * 32 + lane) < tn) pb[i] = __ldcs(gb + i * 32);
         }
       }
     };
@@ -310,12 +324,22 @@ __global__ void __launch_bounds__(WcTile<K, VB, WIDE>::NT, 1)
         }
       } else {
         const Router<K> R = make_router<K>(P, hz, hk);
+        if (WIDE != 0 && use_bid) {
 #pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-          const uint32_t e = warp * WS + i * 32 + lane;
-          bk[i] = 0xFFFFFFFFu;
-          if (e < tn) rank_one(i, R(key[i]));
-          __syncwarp();
+          for (int i = 0; i < IPT; ++i) {
+            const uint32_t e = warp * WS + i * 32 + lane;
+            bk[i] = 0xFFFFFFFFu;
+            if (e < tn) rank_one(i, pb[WIDE ? i : 0]);
+            __syncwarp();
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < IPT; ++i) {
+            const uint32_t e = warp * WS + i * 32 + lane;
+            bk[i] = 0xFFFFFFFFu;
+            if (e < tn) rank_one(i, R(key[i]));
+            __syncwarp();
+          }
         }
       }
       __syncthreads();

@@ -12,7 +12,10 @@ namespace dts {
 // chip-wide, well above the 4-byte-key HBM stream) and store the row into
 // the [bucket][row] count matrix.
 // ---------------------------------------------------------------------------
-template <typename K, int NT, bool SPLIT>
+// KEEP: waves with heavy keys — the bucket ids of heavy segments' records are
+// written to `bid` for the scatter (its own instantiation: the plain path's
+// code, at the copy peak on C2, stays as it is)
+template <typename K, int NT, bool SPLIT, bool KEEP = false>
 __global__ void __launch_bounds__(NT) k_histogram(const SegPlan* __restrict__ plans,
                                                   const Blk* __restrict__ blks, uint32_t nblk,
                                                   uint32_t* __restrict__ ctr,
@@ -21,7 +24,8 @@ __global__ void __launch_bounds__(NT) k_histogram(const SegPlan* __restrict__ pl
                                                   const K* __restrict__ heavy_pool,
                                                   const uint32_t* __restrict__ hz_pool,
                                                   const uint64_t* __restrict__ split_idx,
-                                                  uint64_t global_base, Caps caps) {
+                                                  uint64_t global_base, Caps caps,
+                                                  uint16_t* __restrict__ bid = nullptr) {
   constexpr int VEC = 16 / sizeof(K);
   constexpr int U = 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -53,9 +57,16 @@ __global__ void __launch_bounds__(NT) k_histogram(const SegPlan* __restrict__ pl
     // ATOMS.POPC.INC, which combines a warp instruction's same-address lanes;
     // a per-thread register count of the sampler's hot bucket was measured
     // slower on Zipf 1.5 — the branch costs more than it saves)
-    auto count_one = [&](K key, uint64_t e) {
+    // segments with heavy keys: the bucket ids (zone word, then the zone's
+    // heavy key: two dependent SMEM loads per record) are kept, 2 bytes per
+    // record, for the scatter of the same wave — it ranks from them instead
+    // of routing every record again
+    const bool keep = KEEP && !SPLIT && bid != nullptr && (P.flags & PF_HEAVY);
+    uint16_t* bq = bid + B.begin;
+    auto count_one = [&](K key, uint64_t e) -> uint32_t {
       const uint32_t b = SPLIT ? SR(key, global_base + B.begin + e) : R(key);
       atomicAdd(&hist[b], 1u);
+      return b;
     };
     // partition (<= 8 destinations): 8-bit counters packed in one u64
     // register per thread (a thread counts < 256 keys of a block), reduced
@@ -73,11 +84,24 @@ __global__ void __launch_bounds__(NT) k_histogram(const SegPlan* __restrict__ pl
     const uint64_t nvec = (n - head) / VEC;
     const uint64_t tail0 = head + nvec * VEC;
     if ((uint64_t)tid < head) {
-      if (SPLIT) count_split(p[tid], tid); else count_one(p[tid], tid);
+      if (SPLIT) {
+        count_split(p[tid], tid);
+      } else {
+        const uint32_t b = count_one(p[tid], tid);
+        if (KEEP && keep) bq[tid] = (uint16_t)b;
+      }
     }
     if ((uint64_t)tid < n - tail0) {
-      if (SPLIT) count_split(p[tail0 + tid], tail0 + tid); else count_one(p[tail0 + tid], tail0 + tid);
+      if (SPLIT) {
+        count_split(p[tail0 + tid], tail0 + tid);
+      } else {
+        const uint32_t b = count_one(p[tail0 + tid], tail0 + tid);
+        if (KEEP && keep) bq[tail0 + tid] = (uint16_t)b;
+      }
     }
+    // (the ids of a 16-byte key vector leave as one 8- or 4-byte store when
+    // the id array is aligned like the keys)
+    const bool bvec = keep && ((reinterpret_cast<uint64_t>(bq + head) & (2 * VEC - 1)) == 0);
     const uint4* pv = reinterpret_cast<const uint4*>(p + head);
     for (uint64_t vb = 0; vb < nvec; vb += (uint64_t)NT * U) {
       uint4 v[U];
@@ -97,8 +121,21 @@ __global__ void __launch_bounds__(NT) k_histogram(const SegPlan* __restrict__ pl
           }
         } else if (vi < nvec) {
           const K* kk = reinterpret_cast<const K*>(&v[u]);
+          uint32_t bb[VEC];
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) count_one(kk[e], head + vi * VEC + e);
+          for (int e = 0; e < VEC; ++e) bb[e] = count_one(kk[e], head + vi * VEC + e);
+          if (KEEP && keep) {
+            uint16_t* q = bq + head + vi * VEC;
+            if (bvec) {
+              if constexpr (VEC == 4)
+                *reinterpret_cast<uint2*>(q) = make_uint2(bb[0] | (bb[1] << 16), bb[2] | (bb[3] << 16));
+              else
+                *reinterpret_cast<uint32_t*>(q) = bb[0] | (bb[1] << 16);
+            } else {
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) q[e] = (uint16_t)bb[e];
+            }
+          }
         }
       }
     }
