@@ -31,7 +31,7 @@ for rep in range(2):
     r = sort_device(k, v, SortConfig(), 0, report=True)
     torch.cuda.synchronize()
     L.dts_debug_phases(buf, 16, 0)
-tiles = (r.kernel_records["local_sort"] / 4100.0) if LOCAL else (r.kernel_records["scatter"] / 4608.0)
+tiles = (r.kernel_records["local_sort"] / 4100.0) if LOCAL else (r.kernel_records["scatter"] / 9216.0)
 ctas = buf[14]
 tot = sum(buf[i] for i in range(11))
 print(f"tiles ~{tiles:.0f}  CTA-runs {ctas}  spins {buf[15]}  order-fixes wc {buf[13]} lookback {buf[12]}")
