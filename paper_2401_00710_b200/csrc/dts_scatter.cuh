@@ -307,12 +307,13 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
         __syncwarp();
       }
     } else if (SPLIT) {
-      // few destinations (G ranks): ranks from ballot peer masks; the first
-      // lane of each group bumps the warp's u16 counter (no atomics, so no
-      // same-address serialisation and no reliance on atomic order)
+      // very few destinations (G <= 4 ranks): ranks from ballot peer masks;
+      // the first lane of each group bumps the warp's u16 counter (no
+      // atomics: 8-16 lanes per address would serialise)
       SplitRouter<K> SR;
       SR.sk = hk; SR.si = si; SR.ns = P.nheavy;
       SR.tab = P.nheavy <= 15 ? reinterpret_cast<const uint8_t*>(hz) : nullptr;
+      if (nb <= 4) {
       uint16_t* myc16 = reinterpret_cast<uint16_t*>(mywh);
       const int nbits = nb > 1 ? 32 - __clz((int)(nb - 1)) : 0;
 #pragma unroll
@@ -329,6 +330,21 @@ __global__ void __launch_bounds__(ScatterTile<K, VB>::NT, 2)
         lr[i] = base + before;
         if (valid && before == 0) myc16[b] = (uint16_t)(base + __popc(peers));
         __syncwarp();
+      }
+      } else {
+        // more destinations: the rank atomics of any digit — G destinations
+        // put ~32 / G lanes of a warp instruction on one counter, which the
+        // B200 serves at full rate up to ~5 lanes per address
+        // (tools/mb_atoms.cu), while the ballot peer masks cost 1.3 warp
+        // instructions per record (10^9 records, G = 8: 9.7 -> 8.2 ms, G = 64:
+        // 19.6 -> 16.7; G = 2: 7.8 -> 9.1, hence the ballots above)
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          const uint32_t e = warp * WS + i * 32 + lane;
+          bk[i] = 0xFFFFu;
+          if (e < tn) rank_one(i, SR(sk[e], global_base + g0 + e));
+          __syncwarp();
+        }
       }
     } else {
       const Router<K> R = make_router<K>(P, hz, hk);
