@@ -129,7 +129,14 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
   const uint32_t nspan = *nspan_p;  // device-resident count (k_classify)
   // (one thread's) descriptor of the span after the one in flight: in SMEM —
   // a register copy costs every thread 4 registers of a kernel at its cap
-  __shared__ Span s_next;
+  __shared__ __align__(16) Span s_next;
+  // (fetched by cp.async: a plain load + store would stall the fetching warp
+  // on the global latency in front of its rank atomics, and the block's next
+  // barrier behind it)
+  auto fetch_next = [&](const Span* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;" ::"r"(smem_u32(&s_next)), "l"(src) : "memory");
+  };
+  auto next_ready = [&]() { asm volatile("cp.async.wait_group 0;" ::: "memory"); };
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -141,7 +148,7 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
   __syncthreads();
   if (tid == NT - 1) {
     if (blockIdx.x < nspan) issue(spans[blockIdx.x], 0);
-    if (blockIdx.x + G < nspan) s_next = spans[blockIdx.x + G];
+    if (blockIdx.x + G < nspan) fetch_next(spans + blockIdx.x + G);
   }
   for (uint32_t i = tid; i < (uint32_t)(SL::cnt_bytes / 4); i += NT) cnt[i] = 0u;
   __syncthreads();
@@ -154,8 +161,9 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
     if (TL::SINGLE && sidx != blockIdx.x && tid == NT - 1) {
       // one buffer: every thread is past the previous span's last read (its
       // final barrier), the span's descriptor was fetched an iteration ago
+      next_ready();
       issue(s_next, cur);
-      if (sidx + G < nspan) s_next = spans[sidx + G];
+      if (sidx + G < nspan) fetch_next(spans + sidx + G);
     }
     if (cur == 0) {
       mbar_wait(&bar[0], ph0);
@@ -198,8 +206,11 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
     // stream the next span into the other buffer (freed by the previous
     // iteration's final barrier); fetch the descriptor after it
     if (!TL::SINGLE && tid == NT - 1) {
-      if (sidx + G < nspan) issue(s_next, cur ^ 1);
-      if (sidx + 2 * G < nspan) s_next = spans[sidx + 2 * G];
+      if (sidx + G < nspan) {
+        next_ready();
+        issue(s_next, cur ^ 1);
+      }
+      if (sidx + 2 * G < nspan) fetch_next(spans + sidx + 2 * G);
     }
     if (!known) {
       diff = 0;
