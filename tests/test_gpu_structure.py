@@ -90,3 +90,27 @@ def test_all_equal_keys_leave_in_one_pass():
     keys = np.full(n, 42, np.uint32)
     rep = _dev_sort(keys, np.arange(n, dtype=np.uint32))
     assert rep.heavy_records_removed[0] == n and rep.levels == 1
+
+
+def test_u64_records_reach_the_base_case_after_one_pass_at_3800_per_bucket():
+    """8-byte columns: the base case takes spans of 4608 records (one SMEM span
+    buffer), so 512 buckets of ~3800 u64/u64 records end after ONE distribution
+    pass (with the former 2560-record spans every bucket went down a level)."""
+    rng = np.random.default_rng(11)
+    n = 512 * 3800
+    keys = rng.integers(0, 2**64 - 1, size=n, dtype=np.uint64, endpoint=True)
+    rep = _dev_sort(keys, np.arange(n, dtype=np.uint64))
+    assert rep.levels == 1
+    assert rep.records_distributed == n and rep.base_case_records == n
+
+
+def test_small_duplicate_rich_segments_take_wide_digits():
+    """A segment just above the base case is split on at least 6 bits per
+    level: 40 000 records over 64 distinct values in the low 12 bits leave
+    after one pass, not after a 2-bit-per-level tail of levels."""
+    rng = np.random.default_rng(12)
+    n = 40_000
+    vals64 = rng.integers(0, 4096, size=64).astype(np.uint32)
+    keys = vals64[rng.integers(0, 64, size=n)]
+    rep = _dev_sort(keys, np.arange(n, dtype=np.uint32))
+    assert rep.levels <= 2
