@@ -36,11 +36,10 @@ template <> struct StPair<unsigned long long> {
   __device__ static T make(unsigned long long k, unsigned long long v) { return make_ulonglong2(k, v); }
 };
 
-// WIDE = 1: the variant for heavy-key-rich waves (2^9 zones + up to 43
-// heavy keys + overflow = 600 bucket columns): the carries and per-warp
-// counters grow by 80 columns, paid for with smaller tiles where the two
-// tile buffers would not fit beside them (u32/u32: 12 records per thread,
-// 8-byte pairs: 6)
+// WIDE = 1: the variant for waves with heavy keys (2^9 zones + up to 43
+// heavy keys + overflow = 600 bucket columns: the carries and per-warp
+// counters grow by 80 columns): it ranks heavy segments from the bucket ids
+// k_histogram kept and writes long runs' chunk descriptors with the whole CTA
 template <typename K, int VB, int WIDE = 0> struct WcTile {
   // 512 threads: 768 (16.4 ms) and 1024 measured slower on C2 — the
   // per-bucket phases lengthen with the warp count
@@ -91,13 +90,16 @@ template <typename K, int VB, int WIDE = 0> struct WcSmem {
 
 // ---------------------------------------------------------------------------
 // k_scatter_wc: persistent, one CTA per SM, stripes taken from an atomic
-// counter in input order.  Two SMEM buffers alternate per tile: a tile is
-// streamed in by TMA while the previous one is ranked, and once its records
-// sit in registers its own buffer becomes the staging area.  Per tile:
-//   * ranks: route each key (read from SMEM right before its atomic — this
-//     issue pattern keeps the SMEM atomics of one warp instruction in lane
-//     order; order is verified below anyway) and take per-warp packed u16
-//     counters (k_scatter's scheme);
+// counter in input order.  A tile's records come in by coalesced streaming
+// loads straight into registers, issued right after the previous tile's
+// placement (a TMA bulk prefetch pulls the tile into L2 one tile earlier);
+// the one SMEM tile buffer is the staging area.  The kernel is bound by the
+// SM's load/store pipe (SMEM wavefronts + the 32 B/clk store port,
+// tools/mb_store.cu, tools/mb_mio.cu).  Per tile:
+//   * ranks: route each key and take per-warp packed u16 counters (SMEM
+//     atomicAdd-with-return, k_scatter's scheme; the lane order of one
+//     instruction's same-address atomics is verified below — never seen
+//     violated with one atomic per __syncwarp);
 //   * per bucket pair: prefix over warps, tile counts, and one packed block
 //     scan giving both the tile offsets (tst) and the chunk offsets (sfc) of
 //     carry + run; the owner writes its chunks into the chunk -> bucket map;
