@@ -205,6 +205,22 @@ __global__ void __launch_bounds__(LocalTile<K, VB>::NT, 2)
     PH(1)
     // stream the next span into the other buffer (freed by the previous
     // iteration's final barrier); fetch the descriptor after it
+    if (TL::SINGLE && tid == NT - 1 && sidx + G < nspan) {
+      // one buffer: the next span cannot stream into SMEM yet, but a TMA
+      // bulk prefetch pulls it into L2 while this span is sorted
+      next_ready();
+      const Span N = s_next;
+      if (N.len) {
+        const char* src;
+        uint32_t off;
+        const uint32_t kbytes = tile_span<K>((N.src & 1u) ? Tk : Ak, N.offset, N.len, src, off);
+        prefetch_l2(src, kbytes);
+        if (VB) {
+          const uint32_t vbytes = tile_span<V>((N.src & 1u) ? Tv : Av, N.offset, N.len, src, off);
+          prefetch_l2(src, vbytes);
+        }
+      }
+    }
     if (!TL::SINGLE && tid == NT - 1) {
       if (sidx + G < nspan) {
         next_ready();
