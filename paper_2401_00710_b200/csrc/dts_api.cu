@@ -651,6 +651,10 @@ struct Sorter {
         CUDA_TRY(cudaMemcpyAsync(g_pin_back.p, dplans, pb, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
         std::memcpy(plans.data(), g_pin_back.p, pb);
+      } else {
+        // (DTS_WC=0, a debugging path: the pinned plan staging is rewritten
+        // below — the copies above must have left it)
+        CUDA_TRY(cudaStreamSynchronize(st));
       }
     }
     // the write-combining scatter takes waves whose bucket columns fit its

@@ -32,9 +32,15 @@ for c in range(cases):
         keys = (keys.astype(np.uint64) >> rng.geometric(0.5, size=n).astype(np.uint64).clip(0, 63)).astype(kdt)
     pays = None if pdt is None else np.arange(n, dtype=pdt)
     sorter = dt_sort if rng.random() < 0.8 else plain_msd_sort
+    only = int(sys.argv[sys.argv.index("-only") + 1]) if "-only" in sys.argv else -1
+    seed_c = int(rng.integers(0, 1000))
+    if only >= 0 and c != only:
+        continue
+    if "-v" in sys.argv:
+        print(c, kdt.__name__, None if pdt is None else pdt.__name__, n, bits, kind, sorter.__name__, flush=True)
     order = np.argsort(keys, kind="stable")
     rec = RecordArray(keys.copy(), None if pays is None else pays.copy())
-    sorter(rec, SortConfig(seed=int(rng.integers(0, 1000))))
+    sorter(rec, SortConfig(seed=seed_c))
     ok = np.array_equal(rec.keys, keys[order]) and (pays is None or np.array_equal(rec.payloads, pays[order]))
     if not ok:
         fails += 1
