@@ -1,6 +1,7 @@
-"""GPU: sizes around the write-combining scatter's tile (7168 u32/u32
-records, 3584 for 8-byte columns) and stripe (44 tiles) boundaries, and
-around the local sort's span capacity — bit-exact against the oracle."""
+"""GPU: sizes around the write-combining scatter's tile (9216 records with
+4-byte columns, 5120 with 8-byte columns) and stripe (about 44 tiles)
+boundaries, and around the local sort's span capacity (4608 records) —
+bit-exact against the oracle."""
 import numpy as np
 import pytest
 
@@ -8,9 +9,10 @@ from oracle import oracle as ora
 
 pytestmark = pytest.mark.gpu
 
-T32, T64, LBS = 7168, 3584, 44
-SIZES = sorted({T32 - 1, T32, T32 + 1, T32 * LBS - 1, T32 * LBS, T32 * LBS + 1, 3 * T32 * LBS + 4097,
-                T64 * LBS + 5, 2 * T64 * LBS - 3, 4607, 4608, 4609, 2559, 2560, 2561})
+T32, T64, LBS = 9216, 5120, 44
+SIZES = sorted({T32 - 1, T32, T32 + 1, 2 * T32 - 1, 2 * T32 + 1, T32 * LBS - 1, T32 * LBS, T32 * LBS + 1,
+                3 * T32 * LBS + 4097, T64 - 1, T64, T64 + 1, T64 * LBS + 5, 2 * T64 * LBS - 3,
+                4607, 4608, 4609, 2 * 4608 + 1, 2559, 2560, 2561, 7167, 7168, 7169})
 
 
 @pytest.mark.parametrize("kb,vb", [(4, 4), (8, 8), (4, 0)])
