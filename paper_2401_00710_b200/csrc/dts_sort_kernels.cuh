@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(NT) k_histogram(const SegPlan* __restrict__ pl
     // record, for the scatter of the same wave — it ranks from them instead
     // of routing every record again
     const bool keep = KEEP && !SPLIT && bid != nullptr && (P.flags & PF_HEAVY);
-    uint16_t* bq = bid + B.begin;
+    uint16_t* bq = keep ? bid + B.begin : nullptr;
     auto count_one = [&](K key, uint64_t e) -> uint32_t {
       const uint32_t b = SPLIT ? SR(key, global_base + B.begin + e) : R(key);
       atomicAdd(&hist[b], 1u);
